@@ -1,0 +1,152 @@
+/*
+ * fp8q.h -- C-ABI of libfp8q, the B200 (sm_100a) hot path of the FP8 W8A8 rollout in
+ * "FP8-RL: A Practical and Stable Low-Precision Stack for LLM Reinforcement Learning"
+ * (arXiv 2601.18150).  PAPER.md = /root/reference/PAPER.md (line numbers cited).
+ *
+ * The three operations of the paper's statement of the problem (§2.1):
+ *   quantize_weight_blockwise      Eq. (1): W_hat = round(W / scale), one
+ *                                  scale per 128x128 block from the block's max |W|; done at
+ *                                  every weight synchronisation.
+ *   quantize_act_per_token_group   dynamic activation quantization, one
+ *                                  scale per token per 128 channels (1x128).
+ *   fp8_block_gemm[_grouped]       the W8A8 linear / MoE expert GEMM consuming both
+ *                                  (PAPER.md:62,99,129,147), blockwise scales promoted per
+ *                                  128-deep k-block into an fp32 accumulator.
+ *
+ * Arithmetic (readings fixed in DESIGN.md §3; Q-numbers from SURVEY.md §8(c)):
+ *   E4M3 = OCP E4M3FN (bias 7, no Inf, NaN = S.1111.111, max 448)          (Q9)
+ *   amax  = max |x| over the block/group's in-bounds elements (BF16 widened exactly)
+ *   s     = RN32(amax / 448)  (one IEEE binary32 division); amax == 0 -> s = 1    (Q2,Q4,Q5)
+ *   code  = E4M3_RNE_satfinite(RN32(x / s)); the sign of zero is kept (-0 -> 0x80) (Q1,Q3,Q6,Q7)
+ *   GEMM  D[m,n] = sum_kb (sa[kb][m] * sb[n/128][kb]) * P_kb[m,n],
+ *         P_kb[m,n] = sum_{k in kb} dec(a[m,k]) dec(b[n,k])   (fp32 tensor-core partials,
+ *         fp32 promotion in k-block order, deterministic; BF16 output = RNE of the F32 result)
+ *
+ * Conventions (all entry points):
+ *   - Ownership: the caller owns every buffer; the library never allocates device memory.
+ *     All data pointers are DEVICE pointers unless stated otherwise.
+ *   - Asynchrony: work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream) and the call returns immediately.
+ *   - Validation errors are synchronous: a non-OK status means nothing was enqueued and no
+ *     output was touched.  Device faults surface at the next synchronisation as cudaError.
+ *   - Stateless apart from once-per-process kernel attributes and a cached driver entry
+ *     point; thread-safe.  No C++ exception crosses the ABI.
+ *   - Deterministic: identical inputs give bitwise-identical outputs (no float atomics).
+ *   - Layouts are row-major with an explicit leading dimension in ELEMENTS.
+ */
+#ifndef FP8Q_H_
+#define FP8Q_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FP8Q_OK = 0,
+    FP8Q_EINVAL = 1,       /* null pointer with non-empty extent, negative dim, ld < extent */
+    FP8Q_ESHAPE = 2,       /* k % 128 (act, GEMM), k % 8 (weights), n % 8 (GEMM), bad groups */
+    FP8Q_EALIGN = 3,       /* pointer / leading-dimension alignment required by vector IO/TMA */
+    FP8Q_ECUDA = 4,        /* a CUDA runtime call failed at enqueue time */
+    FP8Q_EUNSUPPORTED = 5, /* device is not sm_100 or a feature is not built */
+    FP8Q_EWORKSPACE = 6    /* workspace smaller than *_workspace_size() */
+} fp8q_status;
+
+typedef enum { FP8Q_OUT_BF16 = 0, FP8Q_OUT_F32 = 1 } fp8q_out_dtype;
+
+/* Human-readable name of a status code (static storage; never NULL). */
+const char* fp8q_status_string(fp8q_status s);
+
+/* Library ABI version (major*10000 + minor*100 + patch). */
+int32_t fp8q_version(void);
+
+/*
+ * quantize_weight_blockwise -- PAPER.md:54-58 (§2.1.1, Eq. (1)); per-step resync PAPER.md:72.
+ *   w_bf16  [n, k] BF16, row stride ld_w (elements).  nn.Linear layout [out = N, in = K].
+ *   codes   [n, k] E4M3 bytes out, row stride ld_q.
+ *   scales  [ceil(n/128), ceil(k/128)] fp32 out, row stride ld_s >= ceil(k/128).
+ *           Block (i, j) covers rows [128i, min(128i+128, n)) x cols [128j, min(128j+128, k));
+ *           ragged edge blocks are clipped (their amax is over in-bounds elements only).
+ *   nonfinite_flag  nullable device int32; set to 1 (never cleared) if any input element is
+ *           NaN/Inf.  The codes/scales of such a block are then unspecified (the oracle
+ *           rejects such input).
+ *   Requirements: n, k >= 0; ld_w >= k, ld_q >= k; k % 8 == 0 (else ESHAPE);
+ *     w_bf16 16-byte aligned, ld_w % 8 == 0; codes 8-byte aligned, ld_q % 8 == 0 (else EALIGN).
+ *   Work: 3 + 4/16384 bytes of HBM traffic per element (2 read, 1 written, 4 per block).
+ */
+fp8q_status quantize_weight_blockwise(const void* w_bf16, int64_t n, int64_t k, int64_t ld_w,
+                                      uint8_t* codes, int64_t ld_q, float* scales, int64_t ld_s,
+                                      int32_t* nonfinite_flag, void* stream);
+
+/*
+ * quantize_act_per_token_group -- dynamic activation quantization, PAPER.md:46,65,73;
+ * granularity 1x128 (per token m, per 128-channel group g).
+ *   x_bf16  [m, k] BF16, row stride ld_x.
+ *   codes   [m, k] E4M3 bytes out, row stride ld_q.
+ *   scales  fp32 out, MN-MAJOR: the scale of (m, g) is scales[g * ld_s + m]; ld_s >= m and
+ *           ld_s % 4 == 0 so every group's column of M scales is a 16-byte aligned row
+ *           (the layout fp8_block_gemm consumes as `a_scales`).
+ *   nonfinite_flag  as above.
+ *   Requirements: k % 128 == 0 (ESHAPE); x_bf16 16-byte aligned, ld_x % 8 == 0, codes 8-byte
+ *     aligned, ld_q % 8 == 0, scales 4-byte aligned, ld_s % 4 == 0 (EALIGN).
+ *   Work: 3 + 4/128 bytes of HBM traffic per element.
+ */
+fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t k, int64_t ld_x,
+                                         uint8_t* codes, int64_t ld_q, float* scales, int64_t ld_s,
+                                         int32_t* nonfinite_flag, void* stream);
+
+/*
+ * fp8_block_gemm -- the W8A8 linear Y = X W^T, blockwise scales promoted
+ * per 128-deep k-block (DeepSeek-V3 granularity cited at PAPER.md:233):
+ *   D[m,n] = sum_kb sa[kb][m] * sb[n/128][kb] * sum_{k in kb} dec(a[m,k]) * dec(b[n,k])
+ *   a        [m, k] E4M3 codes (K-major), row stride ld_a bytes.
+ *   a_scales MN-major [k/128][ld_sa] fp32 (as written by quantize_act_per_token_group).
+ *   b        [n, k] E4M3 codes (K-major, nn.Linear weight), row stride ld_b bytes.
+ *   b_scales [ceil(n/128)][ld_sb] fp32 (as written by quantize_weight_blockwise), ld_sb >= k/128.
+ *   d        [m, n] out, BF16 or F32 per d_dtype, row stride ld_d elements.
+ *   workspace / workspace_bytes: see fp8_block_gemm_workspace_size (currently 0 bytes;
+ *           workspace may be NULL when 0 is required).
+ *   Requirements: k % 128 == 0, n % 8 == 0 (ESHAPE); a, b 16-byte aligned with ld_a % 16 ==
+ *     0 and ld_b % 16 == 0 (TMA); d 16-byte aligned with ld_d * sizeof(out) % 16 == 0;
+ *     a_scales/b_scales 4-byte aligned (EALIGN).  m == 0 or n == 0 is a no-op; k == 0 writes 0.
+ *   Work: 2*m*n*k FLOP on the tensor cores (kind::f8f6f4), m*n*k/128 fp32 promotion FMAs.
+ */
+size_t fp8_block_gemm_workspace_size(int64_t m, int64_t n, int64_t k);
+fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales, int64_t ld_sa,
+                           const uint8_t* b, int64_t ld_b, const float* b_scales, int64_t ld_sb,
+                           void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
+                           int64_t k, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * fp8_block_gemm_grouped -- MoE expert layers in FP8 ("MoE expert layers
+ * (fc1, fc2)").  Group g multiplies A rows [offsets[g], offsets[g+1]) by
+ * B_g = b + g * stride_b (bytes) with scales b_scales + g * stride_sb (elements):
+ *   D[r, n] = fp8_block_gemm(A[r,:], B_g)[n]   for offsets[g] <= r < offsets[g+1].
+ *   offsets_dev  DEVICE int32 [num_groups + 1], offsets[0] = 0, non-decreasing,
+ *                offsets[num_groups] = m_total (the router output stays on the device; no
+ *                host sync).  Violating the precondition is undefined behaviour.
+ *   a_scales     MN-major [k/128][ld_sa] over all m_total rows.
+ *   Requirements as fp8_block_gemm, plus stride_b % 16 == 0, num_groups >= 0.
+ */
+size_t fp8_block_gemm_grouped_workspace_size(int64_t m_total, int64_t n, int64_t k,
+                                             int32_t num_groups);
+fp8q_status fp8_block_gemm_grouped(const uint8_t* a, int64_t ld_a, const float* a_scales,
+                                   int64_t ld_sa, const uint8_t* b, int64_t ld_b, int64_t stride_b,
+                                   const float* b_scales, int64_t ld_sb, int64_t stride_sb,
+                                   void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m_total,
+                                   int64_t n, int64_t k, const int32_t* offsets_dev,
+                                   int32_t num_groups, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
+/*
+ * fp8q_kernel_launches -- number of kernels this library has launched in this process
+ * (monotone counter; used by bench.py to report `gpu_launches`).
+ */
+int64_t fp8q_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FP8Q_H_ */

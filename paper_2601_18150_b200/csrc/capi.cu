@@ -1,0 +1,206 @@
+// capi.cu -- the extern "C" boundary declared in include/fp8q.h: argument validation,
+// status codes, dispatch to the sm_100a kernels.  No allocation, no host sync, no exceptions.
+#include <atomic>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/fp8q.h"
+#include "quant_kernels.h"
+
+namespace {
+
+std::atomic<int64_t> g_launches{0};
+
+inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+fp8q_status check_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return FP8Q_ECUDA;
+    static std::atomic<int> cached[64];  // 0 unknown, 1 ok, 2 unsupported
+    if (dev < 0 || dev >= 64) return FP8Q_EUNSUPPORTED;
+    int c = cached[dev].load();
+    if (c == 0) {
+        int major = 0, minor = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+            return FP8Q_ECUDA;
+        c = (major == 10 && minor == 0) ? 1 : 2;  // built for sm_100a only
+        cached[dev].store(c);
+    }
+    return c == 1 ? FP8Q_OK : FP8Q_EUNSUPPORTED;
+}
+
+fp8q_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FP8Q_OK : FP8Q_ECUDA; }
+
+}  // namespace
+
+extern "C" {
+
+const char* fp8q_status_string(fp8q_status s) {
+    switch (s) {
+        case FP8Q_OK: return "FP8Q_OK";
+        case FP8Q_EINVAL: return "FP8Q_EINVAL: null pointer, negative dimension or leading dimension too small";
+        case FP8Q_ESHAPE: return "FP8Q_ESHAPE: shape constraint violated (k % 128, k % 8, n % 8, groups)";
+        case FP8Q_EALIGN: return "FP8Q_EALIGN: pointer or leading-dimension alignment requirement violated";
+        case FP8Q_ECUDA: return "FP8Q_ECUDA: a CUDA runtime call failed";
+        case FP8Q_EUNSUPPORTED: return "FP8Q_EUNSUPPORTED: device is not sm_100 (B200)";
+        case FP8Q_EWORKSPACE: return "FP8Q_EWORKSPACE: workspace too small";
+    }
+    return "FP8Q_UNKNOWN_STATUS";
+}
+
+int32_t fp8q_version(void) { return 10000; }
+
+int64_t fp8q_kernel_launches(void) { return g_launches.load(); }
+
+fp8q_status quantize_weight_blockwise(const void* w_bf16, int64_t n, int64_t k, int64_t ld_w,
+                                      uint8_t* codes, int64_t ld_q, float* scales, int64_t ld_s,
+                                      int32_t* nonfinite_flag, void* stream) {
+    if (n < 0 || k < 0) return FP8Q_EINVAL;
+    if (ld_w < k || ld_q < k || ld_s < (k + 127) / 128) return FP8Q_EINVAL;
+    if (n == 0 || k == 0) return FP8Q_OK;
+    if (w_bf16 == nullptr || codes == nullptr || scales == nullptr) return FP8Q_EINVAL;
+    if (k % 8 != 0) return FP8Q_ESHAPE;
+    if (!aligned(w_bf16, 16) || ld_w % 8 != 0 || !aligned(codes, 8) || ld_q % 8 != 0 ||
+        !aligned(scales, 4) || (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)))
+        return FP8Q_EALIGN;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_weight_blockwise(static_cast<const uint16_t*>(w_bf16), n, k, ld_w,
+                                                  codes, ld_q, scales, ld_s, nonfinite_flag,
+                                                  static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
+fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t k, int64_t ld_x,
+                                         uint8_t* codes, int64_t ld_q, float* scales, int64_t ld_s,
+                                         int32_t* nonfinite_flag, void* stream) {
+    if (m < 0 || k < 0) return FP8Q_EINVAL;
+    if (ld_x < k || ld_q < k || ld_s < m) return FP8Q_EINVAL;
+    if (k % 128 != 0) return FP8Q_ESHAPE;
+    if (m == 0 || k == 0) return FP8Q_OK;
+    if (x_bf16 == nullptr || codes == nullptr || scales == nullptr) return FP8Q_EINVAL;
+    if (!aligned(x_bf16, 16) || ld_x % 8 != 0 || !aligned(codes, 8) || ld_q % 8 != 0 ||
+        !aligned(scales, 4) || ld_s % 4 != 0 ||
+        (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)))
+        return FP8Q_EALIGN;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_act_per_token_group(static_cast<const uint16_t*>(x_bf16), m, k, ld_x,
+                                                     codes, ld_q, scales, ld_s, nonfinite_flag,
+                                                     static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
+size_t fp8_block_gemm_workspace_size(int64_t, int64_t, int64_t) { return 0; }
+
+size_t fp8_block_gemm_grouped_workspace_size(int64_t, int64_t, int64_t, int32_t) { return 0; }
+
+static fp8q_status gemm_common_checks(const uint8_t* a, int64_t ld_a, const float* a_scales,
+                                      int64_t ld_sa, const uint8_t* b, int64_t ld_b,
+                                      const float* b_scales, int64_t ld_sb, void* d, int64_t ld_d,
+                                      fp8q_out_dtype d_dtype, int64_t m, int64_t n, int64_t k) {
+    if (m < 0 || n < 0 || k < 0) return FP8Q_EINVAL;
+    if (d_dtype != FP8Q_OUT_BF16 && d_dtype != FP8Q_OUT_F32) return FP8Q_EINVAL;
+    if (ld_a < k || ld_b < k || ld_d < n || ld_sa < m || ld_sb < k / 128) return FP8Q_EINVAL;
+    if (k % 128 != 0 || n % 8 != 0) return FP8Q_ESHAPE;
+    if (m == 0 || n == 0) return FP8Q_OK;
+    if (d == nullptr) return FP8Q_EINVAL;
+    if (k == 0) return FP8Q_OK;
+    if (a == nullptr || b == nullptr || a_scales == nullptr || b_scales == nullptr) return FP8Q_EINVAL;
+    const int64_t esz = d_dtype == FP8Q_OUT_F32 ? 4 : 2;
+    if (!aligned(a, 16) || !aligned(b, 16) || ld_a % 16 != 0 || ld_b % 16 != 0 || !aligned(d, 16) ||
+        (ld_d * esz) % 16 != 0 || !aligned(a_scales, 4) || !aligned(b_scales, 4))
+        return FP8Q_EALIGN;
+    if (m > 0x7FFFFFFFLL || n > 0x7FFFFFFFLL || k > 0x7FFFFFFFLL) return FP8Q_EINVAL;
+    return check_device();
+}
+
+static fp8q_status zero_output(void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
+                               void* stream) {
+    const size_t esz = d_dtype == FP8Q_OUT_F32 ? 4 : 2;
+    return from_cuda(cudaMemset2DAsync(d, ld_d * esz, 0, n * esz, m, static_cast<cudaStream_t>(stream)));
+}
+
+fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales, int64_t ld_sa,
+                           const uint8_t* b, int64_t ld_b, const float* b_scales, int64_t ld_sb,
+                           void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
+                           int64_t k, void* workspace, size_t workspace_bytes, void* stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    fp8q_status st = gemm_common_checks(a, ld_a, a_scales, ld_sa, b, ld_b, b_scales, ld_sb, d, ld_d,
+                                        d_dtype, m, n, k);
+    if (st != FP8Q_OK || m == 0 || n == 0) return st;
+    if (k == 0) return zero_output(d, ld_d, d_dtype, m, n, stream);
+    fp8q::GemmArgs g{};
+    g.a = a;
+    g.ld_a = ld_a;
+    g.sa = a_scales;
+    g.ld_sa = ld_sa;
+    g.b = b;
+    g.ld_b = ld_b;
+    g.stride_b = 0;
+    g.sb = b_scales;
+    g.ld_sb = ld_sb;
+    g.stride_sb = 0;
+    g.d = d;
+    g.ld_d = ld_d;
+    g.out_f32 = d_dtype == FP8Q_OUT_F32;
+    g.m = m;
+    g.n = n;
+    g.k = k;
+    g.offsets = nullptr;
+    g.groups = 1;
+    int launched = 0;
+    cudaError_t e = fp8q::launch_fp8_block_gemm(g, static_cast<cudaStream_t>(stream), &launched);
+    g_launches.fetch_add(launched);
+    return from_cuda(e);
+}
+
+fp8q_status fp8_block_gemm_grouped(const uint8_t* a, int64_t ld_a, const float* a_scales,
+                                   int64_t ld_sa, const uint8_t* b, int64_t ld_b, int64_t stride_b,
+                                   const float* b_scales, int64_t ld_sb, int64_t stride_sb,
+                                   void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m_total,
+                                   int64_t n, int64_t k, const int32_t* offsets_dev,
+                                   int32_t num_groups, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    if (num_groups < 0) return FP8Q_ESHAPE;
+    fp8q_status st = gemm_common_checks(a, ld_a, a_scales, ld_sa, b, ld_b, b_scales, ld_sb, d, ld_d,
+                                        d_dtype, m_total, n, k);
+    if (st != FP8Q_OK || m_total == 0 || n == 0 || num_groups == 0) return st;
+    if (offsets_dev == nullptr) return FP8Q_EINVAL;
+    if (!aligned(offsets_dev, 4)) return FP8Q_EALIGN;
+    if (num_groups > 1 && (stride_b < ld_b * n || stride_sb < ((n + 127) / 128) * ld_sb))
+        return FP8Q_EINVAL;
+    if (stride_b % 16 != 0) return FP8Q_EALIGN;
+    if (k == 0) return zero_output(d, ld_d, d_dtype, m_total, n, stream);
+    fp8q::GemmArgs g{};
+    g.a = a;
+    g.ld_a = ld_a;
+    g.sa = a_scales;
+    g.ld_sa = ld_sa;
+    g.b = b;
+    g.ld_b = ld_b;
+    g.stride_b = stride_b;
+    g.sb = b_scales;
+    g.ld_sb = ld_sb;
+    g.stride_sb = stride_sb;
+    g.d = d;
+    g.ld_d = ld_d;
+    g.out_f32 = d_dtype == FP8Q_OUT_F32;
+    g.m = m_total;
+    g.n = n;
+    g.k = k;
+    g.offsets = offsets_dev;
+    g.groups = num_groups;
+    int launched = 0;
+    cudaError_t e = fp8q::launch_fp8_block_gemm(g, static_cast<cudaStream_t>(stream), &launched);
+    g_launches.fetch_add(launched);
+    return from_cuda(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,209 @@
+// quant.cu -- the two E4M3 quantizers of the FP8 W8A8 rollout (arXiv 2601.18150 §2.1.1).
+//
+//   quantize_weight_blockwise     PAPER.md:54-58, Eq. (1): one fp32 scale per 128x128 block.
+//   quantize_act_per_token_group  PAPER.md:65,233: one fp32 scale per token per 128 channels.
+//
+// Both are HBM-bound element maps (3 B of traffic per element).  Design:
+//   * 16-byte vector loads of 8 BF16, every load of a CTA issued before any use (32 KB in
+//     flight per weight block, 16 KB per activation warp group) so HBM sees deep queues;
+//   * amax as an INTEGER max over sign-cleared BF16 bits (__vmaxu2 on packed pairs, then a
+//     redux.sync / shuffle reduction).  Widening BF16 -> fp32 is exact and order-preserving
+//     on |x|, so the max of the bits is the bits of the max; bits >= 0x7F80 flag NaN/Inf;
+//   * s = RN32(amax / 448) by one IEEE division per block (reading Q4), amax == 0 -> 1 (Q5);
+//   * RN32(x / s) per element via the guarded Markstein sequence
+//         r = RN(1/s); q0 = RN(x r); e = fma(-q0, s, x); q1 = fma(e, r, q0)
+//     which gives the same E4M3 code as the IEEE quotient for every block with
+//     amax >= 2^-104 (SURVEY.md §0 finding 4; re-proved on the GPU by the exhaustive
+//     (x, amax) map in tests/test_gpu_exhaustive.py); the sign is re-imposed from x so that
+//     x = -0 still gives -0 (IEEE: -0 / s = -0).  Blocks below the guard use div.rn;
+//   * packed cvt.rn.satfinite.e4m3x2.f32 (RNE, saturating, reading Q1/Q7), 8-byte stores.
+#include <cstdint>
+
+#include "ptx.cuh"
+#include "quant_kernels.h"
+
+namespace fp8q {
+
+namespace {
+
+constexpr uint32_t kAmaxFastGuardBits = 0x0B80u;  // BF16 bits of 2^-104
+constexpr uint32_t kNonFiniteBits = 0x7F80u;      // |x| bits >= this: Inf or NaN
+
+// max over the 8 sign-cleared BF16 bit patterns of a 16-byte vector
+__device__ __forceinline__ uint32_t vec_abs_max_bits(const uint4& v) {
+    const uint32_t m = 0x7FFF7FFFu;
+    uint32_t a = __vmaxu2(__vmaxu2(v.x & m, v.y & m), __vmaxu2(v.z & m, v.w & m));
+    return max(a & 0xFFFFu, a >> 16);
+}
+
+__device__ __forceinline__ float scale_from_amax_bits(uint32_t ab) {
+    // amax == 0 -> 1 (reading Q5); otherwise one IEEE binary32 division (reading Q4)
+    return ab == 0u ? 1.0f : __fdiv_rn(__uint_as_float(ab << 16), 448.0f);
+}
+
+// RN32(x / s) for blocks with amax >= 2^-104 (see header comment), sign taken from x.
+__device__ __forceinline__ float quot_fast(float x, float s, float r) {
+    const float q0 = __fmul_rn(x, r);
+    const float e = __fmaf_rn(-q0, s, x);
+    const float q1 = __fmaf_rn(e, r, q0);
+    return __uint_as_float((__float_as_uint(q1) & 0x7FFFFFFFu) | (__float_as_uint(x) & 0x80000000u));
+}
+
+template <bool kFast>
+__device__ __forceinline__ uint2 encode8(const uint4& v, float s, float r) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t c[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float lo = __uint_as_float(w[i] << 16);
+        const float hi = __uint_as_float(w[i] & 0xFFFF0000u);
+        const float qlo = kFast ? quot_fast(lo, s, r) : __fdiv_rn(lo, s);
+        const float qhi = kFast ? quot_fast(hi, s, r) : __fdiv_rn(hi, s);
+        c[i] = cvt_e4m3x2(qlo, qhi);
+    }
+    return make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+}
+
+// ---------------------------------------------------------------------------------------
+// Weights: one CTA (256 threads) per 128x128 block.  Warp w covers rows 16w..16w+15; in each
+// of its 8 loads, lanes 0-15 read one row's 256 B and lanes 16-31 the next row's, so every
+// load instruction moves two full 256-byte row segments.
+__global__ void __launch_bounds__(256) weight_blockwise_kernel(
+    const uint16_t* __restrict__ w, int64_t n, int64_t k, int64_t ld_w, uint8_t* __restrict__ q,
+    int64_t ld_q, float* __restrict__ scales, int64_t ld_s, int64_t nbk,
+    int32_t* __restrict__ nonfinite_flag) {
+    __shared__ uint32_t red[8];
+    const int64_t blk = blockIdx.x;
+    const int64_t bi = blk / nbk;
+    const int64_t bj = blk - bi * nbk;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t col = bj * 128 + (lane & 15) * 8;
+    const int64_t row0 = bi * 128 + warp * 16 + (lane >> 4);
+    const bool col_ok = col < k;
+
+    uint4 v[8];
+    uint32_t ab = 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t row = row0 + 2 * i;
+        v[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (col_ok && row < n) v[i] = ld_stream_v4(w + row * ld_w + col);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ab = max(ab, vec_abs_max_bits(v[i]));
+    ab = __reduce_max_sync(0xFFFFFFFFu, ab);
+    if (lane == 0) red[warp] = ab;
+    __syncthreads();
+    ab = red[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) ab = max(ab, red[i]);
+
+    const float s = scale_from_amax_bits(ab);
+    if (threadIdx.x == 0) {
+        scales[bi * ld_s + bj] = s;
+        if (ab >= kNonFiniteBits && nonfinite_flag != nullptr) *nonfinite_flag = 1;
+    }
+    if (ab >= kAmaxFastGuardBits) {
+        const float r = __frcp_rn(s);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t row = row0 + 2 * i;
+            if (col_ok && row < n) {
+                const uint2 c = encode8<true>(v[i], s, r);
+                st_stream_v2(q + row * ld_q + col, c.x, c.y);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t row = row0 + 2 * i;
+            if (col_ok && row < n) {
+                const uint2 c = encode8<false>(v[i], s, 0.0f);
+                st_stream_v2(q + row * ld_q + col, c.x, c.y);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Activations: one warp per (token row, chunk of 8 groups = 1024 channels).  Vector j of lane
+// l covers channels chunk*1024 + j*256 + l*8, i.e. group 2j + (l >= 16): each half-warp owns
+// one 128-channel group per j and reduces its amax with 4 xor-shuffles.
+__global__ void __launch_bounds__(256) act_per_token_group_kernel(
+    const uint16_t* __restrict__ x, int64_t m, int64_t k, int64_t ld_x, uint8_t* __restrict__ q,
+    int64_t ld_q, float* __restrict__ scales, int64_t ld_s, int64_t chunks_per_row,
+    int32_t* __restrict__ nonfinite_flag) {
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (item >= m * chunks_per_row) return;
+    const int64_t row = item / chunks_per_row;
+    const int64_t chunk = item - row * chunks_per_row;
+    const int64_t groups = k >> 7;
+    const uint16_t* xr = x + row * ld_x;
+
+    uint4 v[4];
+    bool ok[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t g = chunk * 8 + 2 * j + (lane >> 4);
+        ok[j] = g < groups;
+        v[j] = make_uint4(0u, 0u, 0u, 0u);
+        if (ok[j]) v[j] = ld_stream_v4(xr + g * 128 + (lane & 15) * 8);
+    }
+    uint32_t ab[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ab[j] = vec_abs_max_bits(v[j]);
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ab[j] = max(ab[j], __shfl_xor_sync(0xFFFFFFFFu, ab[j], off));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (!ok[j]) continue;
+        const int64_t g = chunk * 8 + 2 * j + (lane >> 4);
+        const float s = scale_from_amax_bits(ab[j]);
+        if ((lane & 15) == 0) {
+            scales[g * ld_s + row] = s;
+            if (ab[j] >= kNonFiniteBits && nonfinite_flag != nullptr) *nonfinite_flag = 1;
+        }
+        uint2 c;
+        if (ab[j] >= kAmaxFastGuardBits)
+            c = encode8<true>(v[j], s, __frcp_rn(s));
+        else
+            c = encode8<false>(v[j], s, 0.0f);
+        st_stream_v2(q + row * ld_q + g * 128 + (lane & 15) * 8, c.x, c.y);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int64_t ld_w,
+                                    uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
+                                    int32_t* flag, cudaStream_t stream) {
+    const int64_t nbn = (n + 127) / 128, nbk = (k + 127) / 128;
+    const int64_t blocks = nbn * nbk;
+    if (blocks == 0) return cudaSuccess;
+    if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
+    weight_blockwise_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        w, n, k, ld_w, q, ld_q, scales, ld_s, nbk, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, int64_t ld_x,
+                                       uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
+                                       int32_t* flag, cudaStream_t stream) {
+    const int64_t groups = k / 128;
+    const int64_t chunks = (groups + 7) / 8;
+    const int64_t items = m * chunks;
+    if (items == 0) return cudaSuccess;
+    const int64_t blocks = (items + 7) / 8;
+    if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
+    act_per_token_group_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        x, m, k, ld_x, q, ld_q, scales, ld_s, chunks, flag);
+    return cudaGetLastError();
+}
+
+}  // namespace fp8q

@@ -1,0 +1,38 @@
+// quant_kernels.h -- internal launch entry points (C++), wrapped by the C-ABI in capi.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fp8q {
+
+cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int64_t ld_w,
+                                    uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
+                                    int32_t* flag, cudaStream_t stream);
+
+cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, int64_t ld_x,
+                                       uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
+                                       int32_t* flag, cudaStream_t stream);
+
+struct GemmArgs {
+    const uint8_t* a;
+    int64_t ld_a;
+    const float* sa;
+    int64_t ld_sa;
+    const uint8_t* b;
+    int64_t ld_b;
+    int64_t stride_b;  // bytes between groups' B matrices (grouped); ignored if groups == 1
+    const float* sb;
+    int64_t ld_sb;
+    int64_t stride_sb;  // elements between groups' scale grids
+    void* d;
+    int64_t ld_d;
+    bool out_f32;
+    int64_t m, n, k;
+    const int32_t* offsets;  // device [groups + 1] or nullptr (dense)
+    int32_t groups;
+};
+
+// Enqueue the tcgen05 blockwise-scaled FP8 GEMM.  Returns cudaSuccess or the first error.
+cudaError_t launch_fp8_block_gemm(const GemmArgs& args, cudaStream_t stream, int* launches);
+
+}  // namespace fp8q

@@ -1,0 +1,215 @@
+"""Thin Python binding of libfp8q (include/fp8q.h) -- argument marshalling only.
+
+Every step of the hot path runs in the sm_100a kernels behind the C-ABI; this module only
+turns torch tensors (device memory from PyTorch's caching allocator) into pointers, leading
+dimensions and the current CUDA stream.  There is no CPU fallback: if libfp8q.so is missing
+or a tensor is not on a CUDA device, the call raises.
+
+Names follow the C-ABI and the paper (§2.1.1, Eq. (1)).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfp8q.so")
+
+FP8Q_OUT_BF16 = 0
+FP8Q_OUT_F32 = 1
+
+_lock = threading.Lock()
+_lib = None
+
+
+class Fp8qError(RuntimeError):
+    """A libfp8q entry point returned a non-OK fp8q_status."""
+
+
+def load_library() -> ctypes.CDLL:
+    """Load libfp8q.so from the package directory; raise if it was not built."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise Fp8qError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2601_18150_b200.build` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        lib.fp8q_status_string.argtypes = [ctypes.c_int]
+        lib.fp8q_status_string.restype = ctypes.c_char_p
+        lib.fp8q_version.restype = I32
+        lib.fp8q_kernel_launches.restype = I64
+        lib.quantize_weight_blockwise.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
+        lib.quantize_weight_blockwise.restype = ctypes.c_int
+        lib.quantize_act_per_token_group.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
+        lib.quantize_act_per_token_group.restype = ctypes.c_int
+        lib.fp8_block_gemm_workspace_size.argtypes = [I64, I64, I64]
+        lib.fp8_block_gemm_workspace_size.restype = ctypes.c_size_t
+        lib.fp8_block_gemm.argtypes = [P, I64, P, I64, P, I64, P, I64, P, I64, ctypes.c_int,
+                                       I64, I64, I64, P, ctypes.c_size_t, P]
+        lib.fp8_block_gemm.restype = ctypes.c_int
+        lib.fp8_block_gemm_grouped_workspace_size.argtypes = [I64, I64, I64, I32]
+        lib.fp8_block_gemm_grouped_workspace_size.restype = ctypes.c_size_t
+        lib.fp8_block_gemm_grouped.argtypes = [P, I64, P, I64, P, I64, I64, P, I64, I64, P, I64,
+                                               ctypes.c_int, I64, I64, I64, P, I32, P,
+                                               ctypes.c_size_t, P]
+        lib.fp8_block_gemm_grouped.restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def _check(status: int, what: str) -> None:
+    if status != 0:
+        msg = load_library().fp8q_status_string(status).decode()
+        raise Fp8qError(f"{what}: {msg}")
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _cuda2d(t: torch.Tensor, name: str, dtype: torch.dtype) -> torch.Tensor:
+    if not t.is_cuda:
+        raise Fp8qError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != dtype:
+        raise Fp8qError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() != 2 or (t.numel() and t.stride(1) != 1):
+        raise Fp8qError(f"{name} must be 2-D with unit stride in the last dimension")
+    return t
+
+
+def _ld(t: torch.Tensor) -> int:
+    return t.stride(0) if t.shape[0] > 1 else max(t.stride(0), t.shape[1])
+
+
+def kernel_launches() -> int:
+    """Kernels libfp8q has launched in this process (for bench.py's gpu_launches)."""
+    return int(load_library().fp8q_kernel_launches())
+
+
+def version() -> int:
+    return int(load_library().fp8q_version())
+
+
+# ------------------------------------------------------------------------------ quantizers
+def quantize_weight_blockwise(w: torch.Tensor, codes: torch.Tensor | None = None,
+                              scales: torch.Tensor | None = None,
+                              nonfinite_flag: torch.Tensor | None = None, stream=None):
+    """Eq. (1): BF16 [n, k] -> (E4M3 codes uint8 [n, k], fp32 scales
+    [ceil(n/128), ceil(k/128)]), one scale = RN32(amax/448) per 128x128 block."""
+    _cuda2d(w, "w", torch.bfloat16)
+    n, k = w.shape
+    if codes is None:
+        codes = torch.empty((n, k), dtype=torch.uint8, device=w.device)
+    if scales is None:
+        scales = torch.empty(((n + 127) // 128, (k + 127) // 128), dtype=torch.float32, device=w.device)
+    _cuda2d(codes, "codes", torch.uint8)
+    _cuda2d(scales, "scales", torch.float32)
+    if codes.shape != (n, k) or scales.shape[0] < (n + 127) // 128 or scales.shape[1] < (k + 127) // 128:
+        raise Fp8qError("output shape mismatch")
+    flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
+    _check(load_library().quantize_weight_blockwise(
+        w.data_ptr(), n, k, _ld(w), codes.data_ptr(), _ld(codes), scales.data_ptr(), _ld(scales),
+        flag, _stream(stream)), "quantize_weight_blockwise")
+    return codes, scales
+
+
+def act_scales_ld(m: int) -> int:
+    """Leading dimension of the MN-major activation-scale array (>= m, multiple of 4)."""
+    return max(4, (m + 3) // 4 * 4)
+
+
+def quantize_act_per_token_group(x: torch.Tensor, codes: torch.Tensor | None = None,
+                                 scales: torch.Tensor | None = None,
+                                 nonfinite_flag: torch.Tensor | None = None, stream=None):
+    """Dynamic 1x128 activation quantization: BF16 [m, k] -> (codes uint8
+    [m, k], scales fp32 MN-major [k/128, ld_s] with scales[g, m] the scale of token m, group g)."""
+    _cuda2d(x, "x", torch.bfloat16)
+    m, k = x.shape
+    if codes is None:
+        codes = torch.empty((m, k), dtype=torch.uint8, device=x.device)
+    if scales is None:
+        scales = torch.empty((k // 128, act_scales_ld(m)), dtype=torch.float32, device=x.device)
+    _cuda2d(codes, "codes", torch.uint8)
+    _cuda2d(scales, "scales", torch.float32)
+    if codes.shape != (m, k) or scales.shape[0] < k // 128 or scales.shape[1] < m:
+        raise Fp8qError("output shape mismatch")
+    flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
+    _check(load_library().quantize_act_per_token_group(
+        x.data_ptr(), m, k, _ld(x), codes.data_ptr(), _ld(codes), scales.data_ptr(),
+        scales.stride(0) if scales.shape[0] > 1 else scales.shape[1], flag, _stream(stream)),
+        "quantize_act_per_token_group")
+    return codes, scales
+
+
+# ------------------------------------------------------------------------------ GEMMs
+def _out(out, m, n, out_dtype, device):
+    if out is None:
+        out = torch.empty((m, n), dtype=out_dtype, device=device)
+    if out_dtype not in (torch.bfloat16, torch.float32) or out.dtype != out_dtype:
+        raise Fp8qError("out dtype must be torch.bfloat16 or torch.float32")
+    _cuda2d(out, "out", out_dtype)
+    if out.shape != (m, n):
+        raise Fp8qError("out shape mismatch")
+    return out
+
+
+def fp8_block_gemm(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_scales: torch.Tensor,
+                   out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None,
+                   stream=None) -> torch.Tensor:
+    """W8A8 linear Y = X W^T: a codes [m,k], a_scales MN-major [k/128, >=m],
+    b codes [n,k], b_scales [ceil(n/128), >=k/128] -> D [m, n] (BF16 or F32)."""
+    _cuda2d(a, "a", torch.uint8)
+    _cuda2d(b, "b", torch.uint8)
+    _cuda2d(a_scales, "a_scales", torch.float32)
+    _cuda2d(b_scales, "b_scales", torch.float32)
+    m, k = a.shape
+    n, kb = b.shape
+    if kb != k:
+        raise Fp8qError("fp8_block_gemm: inner dimensions differ")
+    out = _out(out, m, n, out_dtype, a.device)
+    ld_sa = a_scales.stride(0) if a_scales.shape[0] > 1 else a_scales.shape[1]
+    ld_sb = b_scales.stride(0) if b_scales.shape[0] > 1 else b_scales.shape[1]
+    _check(load_library().fp8_block_gemm(
+        a.data_ptr(), _ld(a), a_scales.data_ptr(), ld_sa, b.data_ptr(), _ld(b), b_scales.data_ptr(),
+        ld_sb, out.data_ptr(), _ld(out), FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16,
+        m, n, k, None, 0, _stream(stream)), "fp8_block_gemm")
+    return out
+
+
+def fp8_block_gemm_grouped(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor,
+                           b_scales: torch.Tensor, offsets: torch.Tensor,
+                           out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None,
+                           stream=None) -> torch.Tensor:
+    """MoE experts: rows [offsets[g], offsets[g+1]) of a times expert g.
+    b codes [G, n, k]; b_scales [G, ceil(n/128), k/128]; offsets int32 [G+1] on the device."""
+    _cuda2d(a, "a", torch.uint8)
+    _cuda2d(a_scales, "a_scales", torch.float32)
+    if not (b.is_cuda and b.dtype == torch.uint8 and b.dim() == 3 and b.stride(2) == 1):
+        raise Fp8qError("b must be a CUDA uint8 [G, n, k] tensor with unit inner stride")
+    if not (b_scales.is_cuda and b_scales.dtype == torch.float32 and b_scales.dim() == 3 and b_scales.stride(2) == 1):
+        raise Fp8qError("b_scales must be a CUDA float32 [G, nb, kb] tensor")
+    if not (offsets.is_cuda and offsets.dtype == torch.int32 and offsets.dim() == 1 and offsets.is_contiguous()):
+        raise Fp8qError("offsets must be a contiguous CUDA int32 tensor [G+1]")
+    G, n, k = b.shape
+    if offsets.numel() != G + 1:
+        raise Fp8qError("offsets must have num_groups + 1 entries")
+    m = a.shape[0]
+    if a.shape[1] != k:
+        raise Fp8qError("inner dimensions differ")
+    out = _out(out, m, n, out_dtype, a.device)
+    ld_sa = a_scales.stride(0) if a_scales.shape[0] > 1 else a_scales.shape[1]
+    _check(load_library().fp8_block_gemm_grouped(
+        a.data_ptr(), _ld(a), a_scales.data_ptr(), ld_sa, b.data_ptr(), b.stride(1), b.stride(0),
+        b_scales.data_ptr(), b_scales.stride(1), b_scales.stride(0), out.data_ptr(), _ld(out),
+        FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16, m, n, k, offsets.data_ptr(),
+        G, None, 0, _stream(stream)), "fp8_block_gemm_grouped")
+    return out

@@ -1,0 +1,102 @@
+"""The C-ABI library loads and exports every symbol include/fp8q.h declares, and its
+synchronous validation paths return the documented status codes (no GPU needed: these
+return before any CUDA call).  Also: the product package never imports the oracle."""
+import ast
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fp8q.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2601_18150_b200 import build
+    build.build()
+    from paper_2601_18150_b200 import fp8q
+    return fp8q.load_library()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*[A-Za-z_][A-Za-z0-9_ \*]*?\b([a-z0-9_]+)\s*\(", src, flags=re.M)
+    return sorted(set(n for n in names if n not in ("defined",)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for required in ["quantize_weight_blockwise", "quantize_act_per_token_group", "fp8_block_gemm",
+                     "fp8_block_gemm_grouped", "fp8_block_gemm_workspace_size",
+                     "fp8_block_gemm_grouped_workspace_size", "fp8q_status_string", "fp8q_version",
+                     "fp8q_kernel_launches"]:
+        assert required in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_status_strings_and_version(lib):
+    for s in range(7):
+        assert lib.fp8q_status_string(s).startswith(b"FP8Q_")
+    assert lib.fp8q_version() == 10000
+    assert lib.fp8q_kernel_launches() >= 0
+
+
+def test_validation_paths_without_gpu(lib):
+    P = ctypes.c_void_p
+    fake = P(0x10000)  # 16-byte aligned, never dereferenced: validation returns first
+    odd = P(0x10001)
+    # negative dimension -> EINVAL
+    assert lib.quantize_weight_blockwise(fake, -1, 128, 128, fake, 128, fake, 1, None, None) == 1
+    # k % 8 -> ESHAPE
+    assert lib.quantize_weight_blockwise(fake, 4, 12, 12, fake, 12, fake, 1, None, None) == 2
+    # misaligned input -> EALIGN
+    assert lib.quantize_weight_blockwise(odd, 4, 128, 128, fake, 128, fake, 1, None, None) == 3
+    # ld too small -> EINVAL
+    assert lib.quantize_weight_blockwise(fake, 4, 128, 64, fake, 128, fake, 1, None, None) == 1
+    # empty -> OK, nothing enqueued
+    assert lib.quantize_weight_blockwise(None, 0, 128, 128, None, 128, None, 1, None, None) == 0
+    # activations: k % 128 -> ESHAPE, ld_s % 4 -> EALIGN
+    assert lib.quantize_act_per_token_group(fake, 4, 200, 200, fake, 200, fake, 4, None, None) == 2
+    assert lib.quantize_act_per_token_group(fake, 3, 128, 128, fake, 128, fake, 3, None, None) == 3
+    # GEMM: n % 8 -> ESHAPE; k % 128 -> ESHAPE; misaligned ld_a -> EALIGN
+    assert lib.fp8_block_gemm(fake, 128, fake, 4, fake, 128, fake, 1, fake, 12, 0, 4, 12, 128, None, 0, None) == 2
+    assert lib.fp8_block_gemm(fake, 200, fake, 4, fake, 200, fake, 1, fake, 16, 0, 4, 16, 200, None, 0, None) == 2
+    assert lib.fp8_block_gemm(fake, 136, fake, 4, fake, 128, fake, 1, fake, 16, 0, 4, 16, 128, None, 0, None) == 3
+    assert lib.fp8_block_gemm_grouped(fake, 128, fake, 4, fake, 128, 2048, fake, 1, 1, fake, 16, 0,
+                                      4, 16, 128, fake, -1, None, 0, None) == 2
+    assert lib.fp8_block_gemm_workspace_size(8192, 6144, 4096) == 0
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2601_18150_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                tree = ast.parse(open(os.path.join(dirpath, f)).read())
+                for node in ast.walk(tree):
+                    if isinstance(node, ast.Import):
+                        assert not any(a.name.split(".")[0] == "oracle" for a in node.names), f
+                    if isinstance(node, ast.ImportFrom):
+                        assert (node.module or "").split(".")[0] != "oracle", f
+            if f.endswith((".cu", ".cuh", ".h", ".cpp")):
+                for line in open(os.path.join(dirpath, f)):
+                    if line.lstrip().startswith("#include"):
+                        assert "oracle" not in line, (f, line)
+
+
+def test_oracle_never_includes_product_headers():
+    src = open(os.path.join(ROOT, "oracle", "fp8q_oracle.c")).read()
+    assert "#include \"" not in src
+    tree = ast.parse(open(os.path.join(ROOT, "oracle", "__init__.py")).read())
+    for node in ast.walk(tree):
+        if isinstance(node, ast.Import):
+            assert not any(a.name.startswith("paper_2601_18150_b200") for a in node.names)
+        if isinstance(node, ast.ImportFrom):
+            assert not (node.module or "").startswith("paper_2601_18150_b200")

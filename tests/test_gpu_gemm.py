@@ -1,0 +1,177 @@
+"""GPU parity of the blockwise-scaled FP8 GEMM (dense and grouped) against the oracle.
+
+Bar (north_star): relative Frobenius error <= 1e-3 against the fp64
+product of the dequantized operands, on the kernel's F32 output (reading Q16).  Stronger
+checks: the scale-probe GEMM is compared BITWISE with its closed form, BF16 output is
+bitwise RNE of the F32 output, and repeated runs are bitwise identical.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2601_18150_b200 import fp8q
+from tests.helpers import (act_scales_logical, act_scales_mn_from_logical, rel_frobenius,
+                           to_dev_bf16)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3  # north_star: rel. Frobenius <= 1e-3
+
+
+def _operands(m, n, k, seed, kind="normal"):
+    if kind == "normal":
+        xb, wb = synth.qwen3_activation(m, k, seed), synth.qwen3_weight(n, k, seed)
+    else:
+        xb = synth.uniform_bits((m, k), seed, lo=0x3000, hi=0x4400)
+        wb = synth.uniform_bits((n, k), seed + 1, lo=0x3000, hi=0x4400)
+    a, sa = oracle.quantize_act_per_token_group(xb)
+    b, sb = oracle.quantize_weight_blockwise(wb)
+    return a, sa, b, sb
+
+
+def _run(a, sa, b, sb, out_dtype=torch.float32):
+    m = a.shape[0]
+    da = torch.from_numpy(a).cuda()
+    db = torch.from_numpy(b).cuda()
+    dsa = act_scales_mn_from_logical(sa, fp8q.act_scales_ld(m))
+    dsb = torch.from_numpy(sb).cuda()
+    y = fp8q.fp8_block_gemm(da, dsa, db, dsb, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return y
+
+
+@pytest.mark.parametrize("m,n,k,seed", [
+    (4, 256, 256, 0), (4, 256, 256, 1), (4, 256, 256, 2),  # configs[0] (C1)
+    (1, 256, 128, 3), (37, 200, 384, 4), (128, 256, 512, 5), (129, 264, 256, 6),
+    (300, 512, 640, 7), (256, 768, 1024, 8), (513, 1032, 256, 9),
+])
+def test_gemm_small_vs_oracle(m, n, k, seed):
+    a, sa, b, sb = _operands(m, n, k, seed)
+    y = _run(a, sa, b, sb).cpu().numpy()
+    ref = oracle.gemm_rows(a, sa, b, sb)
+    err = rel_frobenius(y, ref)
+    assert err <= TOL, err
+    assert err <= 1e-5  # fp32 promotion of exact partials: ~1e-7
+
+
+def test_gemm_wide_dynamic_range():
+    a, sa, b, sb = _operands(200, 512, 512, 11, kind="uniform")
+    y = _run(a, sa, b, sb).cpu().numpy()
+    assert rel_frobenius(y, oracle.gemm_rows(a, sa, b, sb)) <= 1e-5
+
+
+def test_gemm_scale_probe_bitwise():
+    # every activation group / weight block is the constant +-448*2^e: codes 0x7E/0xFE,
+    # scales exactly 2^e, partials exact, so D has an exact closed form.
+    m, n, k = 160, 512, 1024
+    rng = np.random.default_rng(0)
+    ea = rng.integers(-3, 4, size=(m, k // 128))
+    ew = rng.integers(-3, 4, size=(n // 128, k // 128))
+    sgn_a = rng.choice([-1, 1], size=(m, k // 128))
+    sgn_w = rng.choice([-1, 1], size=(n // 128, k // 128))
+    xa = np.repeat(sgn_a * 448.0 * np.exp2(ea), 128, axis=1).astype(np.float32)
+    xw = np.repeat(np.repeat(sgn_w * 448.0 * np.exp2(ew), 128, 0), 128, 1).astype(np.float32)
+    a, sa = oracle.quantize_act_per_token_group(synth.f32_to_bf16_bits(xa))
+    b, sb = oracle.quantize_weight_blockwise(synth.f32_to_bf16_bits(xw))
+    y = _run(a, sa, b, sb).cpu().numpy().astype(np.float64)
+    coef = (sgn_a[:, None, :] * np.repeat(sgn_w, 128, axis=0)[None, :, :]) * \
+        np.exp2(ea[:, None, :] + np.repeat(ew, 128, axis=0)[None, :, :])
+    want = coef.sum(axis=2) * 128.0 * 448.0 * 448.0
+    assert np.array_equal(y, want)
+
+
+def test_gemm_bf16_is_rne_of_f32_and_deterministic():
+    a, sa, b, sb = _operands(300, 768, 1024, 12)
+    yf = _run(a, sa, b, sb, torch.float32)
+    yb = _run(a, sa, b, sb, torch.bfloat16)
+    assert torch.equal(yb.view(torch.int16), yf.to(torch.bfloat16).view(torch.int16))
+    yf2 = _run(a, sa, b, sb, torch.float32)
+    assert torch.equal(yf.view(torch.int32), yf2.view(torch.int32))
+
+
+@pytest.mark.parametrize("m", [1, 2, 8, 64, 192, 256])
+def test_gemm_decode_shapes(m):
+    # C3: decode-shaped GEMMs at Qwen3-8B o_proj width (K = N = 4096)
+    a, sa, b, sb = _operands(m, 4096, 4096, 20 + m)
+    y = _run(a, sa, b, sb).cpu().numpy()
+    assert rel_frobenius(y, oracle.gemm_rows(a, sa, b, sb)) <= TOL
+
+
+@pytest.mark.parametrize("name", ["qkv", "o", "gate_up", "down"])
+def test_gemm_prefill_full_size_sampled(name):
+    # C2 at full size: M = 8192, sampled rows against the oracle (incl. first/last tile rows)
+    n, k = synth.QWEN3_8B_LINEARS[name]
+    m = 8192
+    a, sa, b, sb = _operands(m, n, k, 0)
+    y = _run(a, sa, b, sb, torch.float32)
+    rows = np.unique(np.concatenate([[0, 127, 128, m - 1], np.random.default_rng(1).integers(0, m, 12)]))
+    ref = oracle.gemm_rows(a, sa, b, sb, rows)
+    got = y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert rel_frobenius(got, ref) <= TOL
+    for i in range(len(rows)):
+        assert rel_frobenius(got[i], ref[i]) <= 1e-4
+
+
+def test_gemm_validation_errors():
+    a = torch.zeros((4, 200), dtype=torch.uint8, device="cuda")  # k % 128 != 0
+    sa = torch.ones((2, 4), dtype=torch.float32, device="cuda")
+    b = torch.zeros((256, 200), dtype=torch.uint8, device="cuda")
+    sb = torch.ones((2, 2), dtype=torch.float32, device="cuda")
+    with pytest.raises(fp8q.Fp8qError, match="SHAPE"):
+        fp8q.fp8_block_gemm(a, sa, b, sb)
+    with pytest.raises(fp8q.Fp8qError):
+        fp8q.fp8_block_gemm(a.cpu(), sa, b, sb)
+
+
+# ------------------------------------------------------------------------------ grouped (C4)
+def _grouped_case(sizes, n, k, seed):
+    off = synth.offsets_from_sizes(np.asarray(sizes))
+    m = int(off[-1])
+    G = len(sizes)
+    a, sa = oracle.quantize_act_per_token_group(synth.qwen3_activation(max(m, 1), k, seed)[:m])
+    bq = [oracle.quantize_weight_blockwise(synth.qwen3_weight(n, k, seed * 1000 + g)) for g in range(G)]
+    b = np.stack([t[0] for t in bq])
+    sb = np.stack([t[1] for t in bq])
+    da = torch.from_numpy(a).cuda()
+    dsa = act_scales_mn_from_logical(sa, fp8q.act_scales_ld(m))
+    y = fp8q.fp8_block_gemm_grouped(da, dsa, torch.from_numpy(b).cuda(), torch.from_numpy(sb).cuda(),
+                                    torch.from_numpy(off).cuda(), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    return a, sa, b, sb, off, y
+
+
+@pytest.mark.parametrize("sizes,n,k", [
+    ([3, 0, 130, 1, 20, 0, 256, 77], 256, 256),
+    ([0, 0, 5], 512, 384),
+    ([129, 1, 128, 255], 264, 128),
+])
+def test_grouped_vs_oracle(sizes, n, k):
+    a, sa, b, sb, off, y = _grouped_case(sizes, n, k, 3)
+    ref = oracle.gemm_grouped_rows(a, sa, b, sb, off)
+    assert rel_frobenius(y.cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("skew", [0.0, 1.2])
+def test_grouped_qwen3_30b_fc1_sampled(skew):
+    # C4: 128 experts, fc1 N = 1536, K = 2048, T = 1024 tokens routed top-8
+    sizes = synth.moe_group_sizes(1024, seed=0, skew=skew)
+    a, sa, b, sb, off, y = _grouped_case(sizes, 1536, 2048, 5)
+    m = int(off[-1])
+    rows = np.unique(np.concatenate([off[1:-1][::9] - 1, np.random.default_rng(2).integers(0, m, 24)]))
+    rows = rows[(rows >= 0) & (rows < m)]
+    ref = oracle.gemm_grouped_rows(a, sa, b, sb, off, rows)
+    got = y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert rel_frobenius(got, ref) <= TOL
+
+
+def test_grouped_equals_dense_per_group_bitwise():
+    # O8: grouped == per-group dense, and the kernel is deterministic -> bitwise equality
+    sizes = [70, 0, 200, 9]
+    a, sa, b, sb, off, y = _grouped_case(sizes, 256, 384, 7)
+    for g in range(len(sizes)):
+        r0, r1 = int(off[g]), int(off[g + 1])
+        if r1 == r0:
+            continue
+        yd = _run(a[r0:r1], sa[r0:r1], b[g], sb[g])
+        assert torch.equal(yd.view(torch.int32), y[r0:r1].contiguous().view(torch.int32))

@@ -1,0 +1,162 @@
+"""GPU parity of the two quantizers against the oracle (bit-exact codes and scales).
+
+PAPER.md:54-58 (Eq. (1), 128x128 weight blocks), PAPER.md:65,233 (dynamic 1x128
+activation groups).  Bar (north_star): FP8 bytes and fp32 scales bit-exact.
+All calls go through the C-ABI (libfp8q.so) via the thin binding.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2601_18150_b200 import fp8q
+from tests.helpers import act_scales_logical, to_dev_bf16, to_host_f32, to_host_u8
+
+pytestmark = pytest.mark.gpu
+
+
+def _weight_case(bits):
+    w = to_dev_bf16(bits)
+    codes, scales = fp8q.quantize_weight_blockwise(w)
+    torch.cuda.synchronize()
+    oc, os_ = oracle.quantize_weight_blockwise(bits)
+    return to_host_u8(codes), to_host_f32(scales), oc, os_
+
+
+def _assert_weight_exact(bits):
+    gc, gs, oc, os_ = _weight_case(bits)
+    assert np.array_equal(gs.view(np.uint32), os_.view(np.uint32)), "scales differ"
+    mism = np.count_nonzero(gc != oc)
+    assert mism == 0, f"{mism} code mismatches"
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_weight_c1_seeds(seed):
+    # configs[0]: single 256x256 BF16 weight, 2x2 blocks of 128
+    _assert_weight_exact(synth.qwen3_weight(256, 256, seed))
+
+
+@pytest.mark.parametrize("n,k", [(300, 200), (129, 136), (1, 8), (128, 128), (131, 392), (640, 1024)])
+def test_weight_ragged_shapes(n, k):
+    _assert_weight_exact(synth.qwen3_weight(n, k, n * 7 + k))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_weight_full_range_bits(seed):
+    # random finite BF16 over the whole range (subnormal ... 3e38), random signs
+    _assert_weight_exact(synth.uniform_bits((384, 512), seed))
+
+
+def test_weight_structured_blocks():
+    n, k = 256, 512
+    x = np.zeros((n, k), np.float32)
+    x[128:, 0:128] = 0.0                       # zero block
+    x[0:128, 128:256] = 1e-38                  # subnormal-scale block (BF16 normal tiny)
+    x[128:256, 256:384] = np.random.default_rng(0).normal(size=(128, 128)) * 1e-3
+    x[130, 300] = 57.0                         # single outlier
+    x[0:128, 384:512] = 2.0 ** -120            # amax below the 2^-104 fast-path guard
+    bits = synth.f32_to_bf16_bits(x)
+    bits[5, 5] = 0x8000                        # -0 inside a zero block
+    bits[200, 0] = 0x8000
+    bits[7, 130] = 0x0001                      # BF16 subnormal element
+    bits[8, 131] = 0x8001
+    _assert_weight_exact(bits)
+
+
+@pytest.mark.parametrize("n,k", [(256, 256), (300, 200), (1024, 768)])
+def test_weight_block_probe(n, k):
+    bits, e = synth.block_probe_bits(n, k, seed=3)
+    gc, gs, oc, os_ = _weight_case(bits)
+    assert np.array_equal(gs, np.exp2(e).astype(np.float32))
+    assert np.array_equal(gc, oc)
+
+
+def test_weight_strided_input_and_outputs():
+    bits = synth.qwen3_weight(256, 384, 9)
+    big = np.zeros((256, 512), np.uint16)
+    big[:, :384] = bits
+    w = to_dev_bf16(big)[:, :384]
+    codes = torch.full((256, 400), 0xAB, dtype=torch.uint8, device="cuda")[:, :384]
+    scales = torch.full((2, 7), -1.0, dtype=torch.float32, device="cuda")[:, :3]
+    fp8q.quantize_weight_blockwise(w, codes, scales)
+    oc, os_ = oracle.quantize_weight_blockwise(bits)
+    assert np.array_equal(to_host_u8(codes), oc)
+    assert np.array_equal(to_host_f32(scales), os_)
+    full = to_host_u8(codes.as_strided((256, 400), (400, 1)))
+    assert np.all(full[:, 384:] == 0xAB)  # padding untouched
+
+
+@pytest.mark.parametrize("name", ["qkv", "down"])
+def test_weight_full_qwen3_8b_shapes(name):
+    n, k = synth.QWEN3_8B_LINEARS[name]
+    _assert_weight_exact(synth.qwen3_weight(n, k, seed=0))
+
+
+def test_weight_moe_expert_stack():
+    # 30B experts: [E][N][K] quantized as one [E*N, K] matrix (N % 128 == 0)
+    e, n, k = 8, 1536, 2048
+    _assert_weight_exact(synth.qwen3_weight(e * n, k, seed=1))
+
+
+def test_nonfinite_flag():
+    bits = synth.qwen3_weight(256, 256, 0)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fp8q.quantize_weight_blockwise(to_dev_bf16(bits), nonfinite_flag=flag)
+    assert int(flag.item()) == 0
+    bits[3, 200] = 0x7F80  # +Inf
+    fp8q.quantize_weight_blockwise(to_dev_bf16(bits), nonfinite_flag=flag)
+    assert int(flag.item()) == 1
+    flag.zero_()
+    x = synth.qwen3_activation(4, 256, 0)
+    x[2, 17] = 0xFFC0  # NaN
+    fp8q.quantize_act_per_token_group(to_dev_bf16(x), nonfinite_flag=flag)
+    assert int(flag.item()) == 1
+
+
+# ------------------------------------------------------------------------------ activations
+def _assert_act_exact(bits, ld_pad=0):
+    m, k = bits.shape
+    x = to_dev_bf16(bits)
+    ld = fp8q.act_scales_ld(m) + ld_pad
+    scales = torch.full((k // 128, ld), -7.0, dtype=torch.float32, device="cuda")
+    codes, scales = fp8q.quantize_act_per_token_group(x, scales=scales)
+    torch.cuda.synchronize()
+    oc, os_ = oracle.quantize_act_per_token_group(bits)
+    gs = act_scales_logical(scales, m)
+    assert np.array_equal(gs.view(np.uint32), os_.view(np.uint32)), "scales differ"
+    mism = np.count_nonzero(to_host_u8(codes) != oc)
+    assert mism == 0, f"{mism} code mismatches"
+    assert np.all(to_host_f32(scales)[:, m:] == -7.0)  # MN-major padding untouched
+
+
+@pytest.mark.parametrize("m,k,seed", [(4, 256, 0), (4, 256, 1), (37, 768, 2), (1, 4096, 3), (64, 12288, 4),
+                                      (129, 2048, 5), (3, 128, 6), (5, 1152, 7)])
+def test_act_shapes(m, k, seed):
+    _assert_act_exact(synth.qwen3_activation(m, k, seed), ld_pad=4)
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_act_full_range_bits(seed):
+    _assert_act_exact(synth.uniform_bits((96, 1024), seed + 10))
+
+
+def test_act_prefill_full_size():
+    # C2 qkv input: M = 8192 tokens x K = 4096
+    _assert_act_exact(synth.qwen3_activation(8192, 4096, 0))
+
+
+def test_act_zero_and_signed_zero_rows():
+    bits = np.zeros((4, 256), np.uint16)
+    bits[1, :] = 0x8000
+    bits[2, 7] = 0x0001
+    bits[3, 255] = 0x8001
+    _assert_act_exact(bits)
+
+
+def test_quantizers_deterministic():
+    bits = synth.qwen3_weight(512, 512, 2)
+    w = to_dev_bf16(bits)
+    c1, s1 = fp8q.quantize_weight_blockwise(w)
+    c2, s2 = fp8q.quantize_weight_blockwise(w)
+    assert torch.equal(c1, c2) and torch.equal(s1, s2)
