@@ -1,0 +1,416 @@
+#!/usr/bin/env python3
+"""bench.py -- the FP8 W8A8 rollout hot path (arXiv 2601.18150 §2.1) on B200.
+
+Default workload (BASELINE.json configs[1], the config the metric is quoted on): one
+Qwen3-8B transformer layer's linear layers at prefill M = 8192 tokens per GPU.  One STEP =
+one pass of the whole hot path:
+  1. weight sync: blockwise requantization of the layer's four BF16 weights
+     (qkv 6144x4096, o 4096x4096, gate_up 24576x4096, down 4096x12288) -- sharded by
+     128-row blocks over the N ranks, then an in-place NCCL all-gather of the FP8 codes and
+     scales (N > 1 only);
+  2. dynamic per-token-group activation quantization of the four GEMM inputs;
+  3. the four blockwise-scaled FP8 GEMMs, BF16 output.
+metric = GEMM TFLOP/s of the whole step (all ranks' GEMM FLOPs / max-over-ranks step time);
+requant GB/s, activation-quant GB/s and GEMM-only TFLOP/s are reported alongside.
+
+Timing (B200_PROFILING.md): W untimed warm-up steps; K timed steps, each bracketed by CUDA
+events on the launching stream; L2 flushed (256 MiB write) between timed steps, outside the
+events; barrier + synchronize on both sides; max over ranks; nvidia-smi clocks sampled
+during the timed region.  `e2e` repeats the step through the same C-ABI calls with HOST
+(pinned) inputs: H2D of the step's BF16 weight shards and activations and D2H of the GEMM
+outputs are inside its timed region.
+
+--impl reference times the CPU oracle (the reference arm of this tier; it is deliberately
+slow) on a bounded sample of the same workload.  Other workloads (--workload sync30b,
+decode, moe) print their own lines for the other configs.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "blockwise-FP8 GEMM TFLOP/s (Qwen3-8B shapes); weight requant GB/s vs HBM"
+M_PREFILL = 8192
+WEIGHT_BYTES_PER_ELEM = 3.0 + 4.0 / 16384  # 2 B read + 1 B code + 4 B scale per 128x128
+ACT_BYTES_PER_ELEM = 3.0 + 4.0 / 128
+
+
+# ----------------------------------------------------------------------------- helpers
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "bf16_tflops": float(p["bf16_tflops"]),
+                "bf16_tflops_sustained": float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+def fp8_peak_tflops(peaks):
+    # FP8 dense = 2x BF16 dense (nominal 4.5 / 2.25 PFLOP/s), applied to the measured BF16 peak
+    return 2.0 * peaks["bf16_tflops"]
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons at 200 ms while the timed region runs."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        p = torch.cuda.get_device_properties(device_index)
+        self.gpu = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [r for r in rows if r[2] > 250.0] or rows
+        names = ["active_mask", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3]) if i > 0 and v == "Active"})
+        return {"sm_mhz": float(np.median([r[0] for r in loaded])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_max": max(r[2] for r in rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- workload
+LAYER = [("qkv",) + synth.QWEN3_8B_LINEARS["qkv"], ("o",) + synth.QWEN3_8B_LINEARS["o"],
+         ("gate_up",) + synth.QWEN3_8B_LINEARS["gate_up"], ("down",) + synth.QWEN3_8B_LINEARS["down"]]
+
+
+def layer_flops(m):
+    return sum(2.0 * m * n * k for _, n, k in LAYER)
+
+
+def bf16_from_bits(bits: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16)
+
+
+class LayerStep:
+    """Device buffers and the step of the default workload on one rank."""
+
+    def __init__(self, world, rank, device, m=M_PREFILL):
+        from paper_2601_18150_b200 import fp8q
+        from paper_2601_18150_b200.sync import TensorSpec, WeightSyncEngine
+        self.fp8q = fp8q
+        self.m = m
+        self.device = device
+        self.world = world
+        specs = [TensorSpec(name, n, k) for name, n, k in LAYER]
+        self.engine = WeightSyncEngine(specs, device)
+        # host (pinned) BF16 weight shards and activations, from the seeded generators
+        self.h_w, self.h_x = {}, {}
+        for i, (name, n, k) in enumerate(LAYER):
+            r0, r1 = self.engine.shard_rows(name)
+            full = synth.qwen3_weight(n, k, seed=i)
+            self.h_w[name] = bf16_from_bits(full[r0:r1]).pin_memory()
+            self.h_x[name] = bf16_from_bits(synth.qwen3_activation(m, k, seed=100 * rank + i)).pin_memory()
+        self.w = {k: v.to(device) for k, v in self.h_w.items()}
+        self.x = {k: v.to(device) for k, v in self.h_x.items()}
+        self.xq, self.xs, self.y = {}, {}, {}
+        for name, n, k in LAYER:
+            self.xq[name] = torch.empty((m, k), dtype=torch.uint8, device=device)
+            self.xs[name] = torch.empty((k // 128, fp8q.act_scales_ld(m)), dtype=torch.float32, device=device)
+            self.y[name] = torch.empty((m, n), dtype=torch.bfloat16, device=device)
+        self.h_y = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in self.y.items()}
+        self.comm = torch.cuda.Stream(device) if world > 1 else None
+        self.step_id = 0
+        self.weight_elems_local = sum(v.numel() for v in self.w.values())
+        self.act_elems = sum(v.numel() for v in self.x.values())
+
+    def run(self, ev=None):
+        fq = self.fp8q
+        self.step_id += 1
+        self.engine.sync_step(self.step_id, self.w, self.comm)
+        if ev:
+            ev[1].record()
+        for name, _, _ in LAYER:
+            fq.quantize_act_per_token_group(self.x[name], self.xq[name], self.xs[name])
+        if ev:
+            ev[2].record()
+        for name, _, _ in LAYER:
+            fq.fp8_block_gemm(self.xq[name], self.xs[name], self.engine.codes[name], self.engine.scales[name],
+                              out=self.y[name])
+
+    def run_e2e(self):
+        for name in self.w:
+            self.w[name].copy_(self.h_w[name], non_blocking=True)
+            self.x[name].copy_(self.h_x[name], non_blocking=True)
+        self.run()
+        for name in self.y:
+            self.h_y[name].copy_(self.y[name], non_blocking=True)
+
+    def h2d_bytes(self):
+        return sum(v.numel() * 2 for v in self.h_w.values()) + sum(v.numel() * 2 for v in self.h_x.values())
+
+    def d2h_bytes(self):
+        return sum(v.numel() * 2 for v in self.h_y.values())
+
+
+_ORACLE_INPUTS = {}
+
+
+def oracle_inputs(rows):
+    """Seeded host inputs for the oracle sample (generated once per process)."""
+    if rows not in _ORACLE_INPUTS:
+        _ORACLE_INPUTS[rows] = [(synth.qwen3_weight(n, k, seed=i), synth.qwen3_activation(rows, k, seed=i))
+                                for i, (_, n, k) in enumerate(LAYER)]
+    return _ORACLE_INPUTS[rows]
+
+
+def cpu_oracle_sample(rows=8):
+    """The oracle as it stands on the host cores: full requant of the layer's weights plus
+    activation quant + fp64 GEMM of `rows` of the M token rows; returns timings."""
+    import oracle
+    nth = oracle.default_threads()
+    t_w = 0.0
+    t_rows = 0.0
+    for wb, xb in oracle_inputs(rows):
+        t0 = time.perf_counter()
+        bq, bs = oracle.quantize_weight_blockwise(wb, nthreads=nth)
+        t1 = time.perf_counter()
+        aq, as_ = oracle.quantize_act_per_token_group(xb, nthreads=nth)
+        oracle.gemm_rows(aq, as_, bq, bs, nthreads=nth)
+        t2 = time.perf_counter()
+        t_w += t1 - t0
+        t_rows += t2 - t1
+    return t_w, t_rows, nth
+
+
+def oracle_value(t_w, t_rows, rows, m=M_PREFILL):
+    full = t_w + t_rows * (m / rows)
+    return layer_flops(m) / full / 1e12, full
+
+
+# ----------------------------------------------------------------------------- arms
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    rows = 2
+    for _ in range(args.warmup):
+        cpu_oracle_sample(rows=rows)
+    tw = tr = 0.0
+    nth = 1
+    for _ in range(args.steps):
+        a, b, nth = cpu_oracle_sample(rows=rows)
+        tw += a
+        tr += b
+    val, full_s = oracle_value(tw / args.steps, tr / args.steps, rows)
+    sample = (f"per step: full blockwise requant of the 4 Qwen3-8B layer weights (193M elements) + "
+              f"activation quant and fp64 GEMM of {rows} of {M_PREFILL} token rows; extrapolated to M={M_PREFILL}")
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(full_s * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded)",
+            "config": {"workload": "qwen3_8b_layer_linears_prefill_m8192", "tokens_per_gpu": M_PREFILL},
+            "cpu_baseline": {"value": round(val, 6), "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(val, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_layer(args):
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(device)
+    peaks = load_peaks()
+    from paper_2601_18150_b200 import fp8q
+    fp8q.load_library()
+    st = LayerStep(world, rank, device)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+
+    for _ in range(args.warmup):
+        st.run()
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    clocks = ClockSampler(device.index)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = fp8q.kernel_launches()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps, outside the events
+        evs[i][0].record()
+        st.run(evs[i])
+        evs[i][3].record()
+    torch.cuda.synchronize()
+    launches = fp8q.kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t_step = [evs[i][0].elapsed_time(evs[i][3]) for i in range(args.steps)]
+    t_sync = [evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps)]
+    t_act = [evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps)]
+    t_gemm = [evs[i][2].elapsed_time(evs[i][3]) for i in range(args.steps)]
+    tot = torch.tensor([sum(t_step)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ms_per_step = total_ms / args.steps
+
+    flops_rank = layer_flops(st.m)
+    value = flops_rank * world / (ms_per_step * 1e-3) / 1e12
+    gemm_ms = float(np.mean(t_gemm))
+    gemm_tflops = flops_rank / (gemm_ms * 1e-3) / 1e12
+    peak = fp8_peak_tflops(peaks)
+    sync_ms = float(np.mean(t_sync))
+    act_ms = float(np.mean(t_act))
+    requant_gbs = st.weight_elems_local * WEIGHT_BYTES_PER_ELEM / (sync_ms * 1e-3) / 1e9
+    act_gbs = st.act_elems * ACT_BYTES_PER_ELEM / (act_ms * 1e-3) / 1e9
+
+    # e2e through the same C-ABI calls with host (pinned) buffers
+    e2e_ms = None
+    if not args.no_e2e:
+        for _ in range(2):
+            st.run_e2e()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            st.run_e2e()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item()) / args.steps
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("fp8_block_gemm_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp8_e4m3 (fp32 accumulate)", "data": "synthetic (seeded Qwen3-8B-shaped BF16 weights/activations)",
+        "config": {"workload": "qwen3_8b_layer_linears_prefill_m8192", "tokens_per_gpu": st.m,
+                   "global_batch": st.m * world, "gemms": {n: [st.m, nn, k] for n, nn, k in LAYER},
+                   "out_dtype": "bf16", "l2": "flushed by a 256 MiB write between timed steps",
+                   "parallelism": f"dp{world}: per-step weight requant sharded by 128-row blocks"
+                                  + (" + NCCL all-gather of FP8 codes/scales" if world > 1 else "")},
+        "breakdown": {"sync_ms": round(sync_ms, 4), "requant_gbs_local": round(requant_gbs, 1),
+                      "requant_frac_hbm": round(requant_gbs / peaks["hbm_gbs"], 4) if world == 1 else None,
+                      "act_quant_ms": round(act_ms, 4), "act_quant_gbs": round(act_gbs, 1),
+                      "act_quant_frac_hbm": round(act_gbs / peaks["hbm_gbs"], 4),
+                      "gemm_ms": round(gemm_ms, 4), "gemm_tflops": round(gemm_tflops, 1),
+                      "gemm_frac_fp8_peak": round(gemm_tflops / peak, 4)},
+        "roofline": {"bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+                     "frac": round(gemm_tflops / peak, 4), "traffic": traffic,
+                     "kernel": "fp8_block_gemm (4 launches/step; achieved = algorithmic GEMM FLOPs / CUDA-event time)",
+                     "peak_source": "2 x bf16 burst of " + peaks["source"]},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if e2e_ms is not None:
+        line["e2e"] = {"value": round(flops_rank * world / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": int(st.h2d_bytes()), "d2h_bytes_per_step": int(st.d2h_bytes()),
+                       "ms_per_step": round(e2e_ms, 3)}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        rows = 8
+        t_w, t_rows, nth = cpu_oracle_sample(rows=rows)
+        val, full_s = oracle_value(t_w, t_rows, rows)
+        line["cpu_baseline"] = {"value": round(val, 8), "unit": "TFLOP/s", "cores": nth, "kind": "oracle",
+                                "sample": f"full requant of the 4 layer weights ({t_w:.2f} s) + act quant and fp64 "
+                                          f"GEMM of {rows}/{M_PREFILL} token rows ({t_rows:.2f} s), extrapolated to "
+                                          f"one full step = {full_s:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["layer8b"], default="layer8b")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_layer(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -48,6 +48,7 @@ constexpr int NUM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 constexpr int TMEM_COLS = 512;  // 2 partial buffers x 256 fp32 columns
 constexpr int NUM_EPI_WARPS = 8;
+constexpr int RASTER_GM = 16;  // m-tiles per raster band
 constexpr uint32_t IDESC = idesc_e4m3_f32(BM, BN);
 constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
 
@@ -98,9 +99,15 @@ struct TileCursor {
             if (++g >= p.groups) return false;
             load(p);
         }
+        // Grouped raster: bands of RASTER_GM m-tiles; inside a band m is fastest, so the ~148
+        // concurrent tiles cover a compact RASTER_GM x ~9 block of the output and both the A
+        // band and the B tiles they touch stay L2-resident (K = 12288 would otherwise re-read A).
         const int64_t l = t - base;
-        mt = static_cast<int>(l % mtiles);
-        nt = static_cast<int>(l / mtiles);
+        const int64_t band = l / (int64_t(RASTER_GM) * p.num_n_tiles);
+        const int64_t r = l - band * (int64_t(RASTER_GM) * p.num_n_tiles);
+        const int64_t gm = min(int64_t(RASTER_GM), mtiles - band * RASTER_GM);
+        mt = static_cast<int>(band * RASTER_GM + r % gm);
+        nt = static_cast<int>(r / gm);
         return true;
     }
 };
@@ -223,11 +230,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const float* sbp = p.sb + int64_t(cur.g) * p.stride_sb + nb * p.ld_sb;
 #pragma unroll
             for (int j = 0; j < 64; ++j) acc[j] = make_float2(0.f, 0.f);
-            float f_next = live ? __ldg(sap) * __ldg(sbp) : 0.f;
+            // Scale prefetch two k-blocks ahead; the raw values are only multiplied when used,
+            // so the load latency never sits between the TMEM-full wait and the FMAs.
+            float sa0 = 0.f, sb0 = 0.f, sa1 = 0.f, sb1 = 0.f;
+            if (live) {
+                sa0 = __ldg(sap);
+                sb0 = __ldg(sbp);
+                if (p.num_kb > 1) {
+                    sa1 = __ldg(sap + p.ld_sa);
+                    sb1 = __ldg(sbp + 1);
+                }
+            }
             for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-                const float f = f_next;
-                if (kb + 1 < p.num_kb)
-                    f_next = live ? __ldg(sap + int64_t(kb + 1) * p.ld_sa) * __ldg(sbp + kb + 1) : 0.f;
+                const float f = sa0 * sb0;
+                sa0 = sa1;
+                sb0 = sb1;
+                if (live && kb + 2 < p.num_kb) {
+                    sa1 = __ldg(sap + int64_t(kb + 2) * p.ld_sa);
+                    sb1 = __ldg(sbp + kb + 2);
+                }
                 const uint32_t buf = it & 1u;
                 const uint32_t bph = (it >> 1) & 1u;
                 mbar_wait(&tfull[buf], bph);

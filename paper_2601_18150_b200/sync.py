@@ -1,0 +1,168 @@
+"""Sharded per-step weight synchronisation (§2.1.2, lines 67-75; SURVEY §8(a) a4,
+§8(e)): "At each RL step, BF16/FP16 weights are retrieved from the training backend ...,
+quantized to FP8 using the blockwise scheme ..., and loaded into the inference engine"
+(PAPER.md:72).
+
+B200 design: with P ranks (one process per GPU), rank r owns a contiguous
+range of 128-row block-rows of every dense weight (or a contiguous range of experts of every
+MoE weight), exactly the slice an FSDP-style sharded trainer holds.  Each rank quantizes
+ONLY its slice, straight into its slot of the persistent full-size FP8 engine buffers, then
+one in-place all-gather per buffer (NCCL over NVLink) fills the other slots.  Block-aligned
+shards are independent, so the gathered bytes equal quantizing the full weight (reading Q17,
+checked bitwise in the tests), and FP8 is gathered instead of BF16 (half the NVLink bytes).
+
+Host logic here (planning, step tags, collectives) is plain Python over torch.distributed;
+the quantizer is the libfp8q kernel.  `quantize_fn` is injectable only so the CPU gloo tests
+can exercise the sharding and gather layout without a GPU.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+BLOCK = 128
+
+
+class StaleStepError(RuntimeError):
+    """sync_step called with a step not newer than the loaded one."""
+
+
+@dataclasses.dataclass(frozen=True)
+class TensorSpec:
+    """One quantized linear weight.  Dense: [n, k] (nn.Linear [out, in]).  MoE experts:
+    experts > 0 and the weight is [experts, n, k] (stored as [experts * n, k])."""
+    name: str
+    n: int
+    k: int
+    experts: int = 0
+
+    @property
+    def rows(self) -> int:
+        return self.n * max(self.experts, 1)
+
+    @property
+    def scale_rows(self) -> int:
+        return max(self.experts, 1) * ((self.n + BLOCK - 1) // BLOCK)
+
+    @property
+    def scale_cols(self) -> int:
+        return (self.k + BLOCK - 1) // BLOCK
+
+
+@dataclasses.dataclass(frozen=True)
+class Shard:
+    """Rows [row0, row1) of the (flattened) weight and scale rows [srow0, srow1) on one rank."""
+    row0: int
+    row1: int
+    srow0: int
+    srow1: int
+
+
+def plan_shards(spec: TensorSpec, world: int) -> List[Shard]:
+    """Split a weight into `world` equal, 128-row-block-aligned shards.
+
+    Dense: rank r gets block-rows [r*B/P, (r+1)*B/P) with B = ceil(n/128) (requires B % P == 0
+    so every rank's slot has the same size for the in-place all-gather; finding 10 of the
+    survey: every Qwen3 fused tensor satisfies this for P <= 8).  MoE: rank r gets experts
+    [r*E/P, (r+1)*E/P) (E % P == 0)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if spec.experts:
+        if spec.experts % world:
+            raise ValueError(f"{spec.name}: {spec.experts} experts not divisible by {world} ranks")
+        if spec.n % BLOCK:
+            raise ValueError(f"{spec.name}: expert rows {spec.n} must be a multiple of {BLOCK}")
+        per = spec.experts // world
+        sb = spec.n // BLOCK
+        return [Shard(r * per * spec.n, (r + 1) * per * spec.n, r * per * sb, (r + 1) * per * sb)
+                for r in range(world)]
+    nb = (spec.n + BLOCK - 1) // BLOCK
+    if nb % world:
+        raise ValueError(f"{spec.name}: {nb} block-rows not divisible by {world} ranks")
+    if world > 1 and spec.n % BLOCK:
+        raise ValueError(f"{spec.name}: sharded weights need n % {BLOCK} == 0")
+    per = nb // world
+    return [Shard(r * per * BLOCK, min((r + 1) * per * BLOCK, spec.n), r * per, (r + 1) * per)
+            for r in range(world)]
+
+
+QuantizeFn = Callable[[torch.Tensor, torch.Tensor, torch.Tensor], None]
+
+
+def _default_quantize(w: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor) -> None:
+    from .fp8q import quantize_weight_blockwise
+    quantize_weight_blockwise(w, codes, scales)
+
+
+class WeightSyncEngine:
+    """Persistent FP8 engine buffers (codes + scales) for a set of weights, refreshed every
+    RL step from this rank's BF16 shards (versioned snapshot, stale-step
+    rejection, post-state equals quantize(snapshot) bitwise)."""
+
+    def __init__(self, specs: Sequence[TensorSpec], device, group=None,
+                 quantize_fn: Optional[QuantizeFn] = None):
+        self.specs = list(specs)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = torch.device(device)
+        self.quantize_fn = quantize_fn or _default_quantize
+        self.plans: Dict[str, List[Shard]] = {s.name: plan_shards(s, self.world) for s in self.specs}
+        self.codes: Dict[str, torch.Tensor] = {}
+        self.scales: Dict[str, torch.Tensor] = {}
+        for s in self.specs:
+            self.codes[s.name] = torch.empty((s.rows, s.k), dtype=torch.uint8, device=self.device)
+            self.scales[s.name] = torch.empty((s.scale_rows, s.scale_cols), dtype=torch.float32,
+                                              device=self.device)
+        self.loaded_step = -1
+
+    def my_shard(self, name: str) -> Shard:
+        return self.plans[name][self.rank]
+
+    def shard_rows(self, name: str) -> Tuple[int, int]:
+        sh = self.my_shard(name)
+        return sh.row0, sh.row1
+
+    def quantize_local(self, name: str, w_shard: torch.Tensor) -> None:
+        """Quantize this rank's BF16 shard straight into its slot of the full buffers."""
+        sh = self.my_shard(name)
+        if w_shard.shape[0] != sh.row1 - sh.row0:
+            raise ValueError(f"{name}: shard has {w_shard.shape[0]} rows, plan says {sh.row1 - sh.row0}")
+        self.quantize_fn(w_shard, self.codes[name][sh.row0:sh.row1], self.scales[name][sh.srow0:sh.srow1])
+
+    def gather(self, name: str, async_op: bool = False):
+        """In-place all-gather of codes and scales: every rank ends with the full FP8 weight."""
+        if self.world == 1:
+            return []
+        sh = self.my_shard(name)
+        c, s = self.codes[name], self.scales[name]
+        h1 = dist.all_gather_into_tensor(c, c[sh.row0:sh.row1], group=self.group, async_op=async_op)
+        h2 = dist.all_gather_into_tensor(s, s[sh.srow0:sh.srow1], group=self.group, async_op=async_op)
+        return [h for h in (h1, h2) if h is not None]
+
+    def sync_step(self, step: int, shards: Dict[str, torch.Tensor], comm_stream=None) -> None:
+        """One weight synchronisation: quantize every local shard, all-gather.
+        With a comm stream, tensor i's gather overlaps tensor i+1's quantization."""
+        if step <= self.loaded_step:
+            raise StaleStepError(f"step {step} is not newer than loaded step {self.loaded_step}")
+        missing = [s.name for s in self.specs if s.name not in shards]
+        if missing:
+            raise KeyError(f"missing shards: {missing}")
+        if comm_stream is None or self.world == 1:
+            for s in self.specs:
+                self.quantize_local(s.name, shards[s.name])
+                self.gather(s.name)
+        else:
+            compute = torch.cuda.current_stream(self.device)
+            for s in self.specs:
+                self.quantize_local(s.name, shards[s.name])
+                ev = torch.cuda.Event()
+                ev.record(compute)
+                with torch.cuda.stream(comm_stream):
+                    comm_stream.wait_event(ev)
+                    self.gather(s.name)
+            compute.wait_stream(comm_stream)
+        self.loaded_step = step

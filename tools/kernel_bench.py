@@ -1,0 +1,106 @@
+#!/usr/bin/env python3
+"""Per-kernel timing sweep (CUDA events on the launching stream, L2 flushed between
+iterations, median of N) for the three libfp8q kernels on the BASELINE.json shapes.
+Development tool: bench.py is the contract; this prints one JSON line per case."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2601_18150_b200 import fp8q  # noqa: E402
+
+PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+HBM = PEAKS["hbm_gbs"]
+FP8 = 2 * PEAKS["bf16_tflops"]
+
+
+def timeit(fn, iters, flush):
+    ts = []
+    for _ in range(3):
+        fn()
+    for _ in range(iters):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts)), float(np.percentile(ts, 10)), float(np.percentile(ts, 90))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--what", default="all")
+    ap.add_argument("--decode", action="store_true")
+    ap.add_argument("--moe", action="store_true")
+    args = ap.parse_args()
+    dev = torch.device("cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    M = 8192
+    for name, (n, k) in synth.QWEN3_8B_LINEARS.items():
+        w = (torch.randn((n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+        x = torch.randn((M, k), generator=g, device=dev).to(torch.bfloat16)
+        wq, ws = fp8q.quantize_weight_blockwise(w)
+        xq, xs = fp8q.quantize_act_per_token_group(x)
+        y = torch.empty((M, n), dtype=torch.bfloat16, device=dev)
+        if args.what in ("all", "wq"):
+            t, lo, hi = timeit(lambda: fp8q.quantize_weight_blockwise(w, wq, ws), args.iters, flush)
+            gbs = n * k * (3 + 4 / 16384) / (t * 1e-3) / 1e9
+            print(json.dumps({"kernel": "quantize_weight_blockwise", "shape": [n, k], "ms": round(t, 4),
+                              "p10": round(lo, 4), "p90": round(hi, 4), "GBps": round(gbs, 1), "frac_hbm": round(gbs / HBM, 4)}))
+        if args.what in ("all", "aq"):
+            t, lo, hi = timeit(lambda: fp8q.quantize_act_per_token_group(x, xq, xs), args.iters, flush)
+            gbs = M * k * (3 + 4 / 128) / (t * 1e-3) / 1e9
+            print(json.dumps({"kernel": "quantize_act_per_token_group", "shape": [M, k], "ms": round(t, 4),
+                              "p10": round(lo, 4), "p90": round(hi, 4), "GBps": round(gbs, 1), "frac_hbm": round(gbs / HBM, 4)}))
+        if args.what in ("all", "gemm"):
+            t, lo, hi = timeit(lambda: fp8q.fp8_block_gemm(xq, xs, wq, ws, out=y), args.iters, flush)
+            tf = 2 * M * n * k / (t * 1e-3) / 1e12
+            print(json.dumps({"kernel": "fp8_block_gemm", "shape": [M, n, k], "ms": round(t, 4), "p10": round(lo, 4),
+                              "p90": round(hi, 4), "TFLOPs": round(tf, 1), "frac_fp8": round(tf / FP8, 4)}))
+        if args.decode:
+            for m in (1, 8, 64, 128, 256):
+                xd = xq[:m]
+                sd = xs[:, :m].contiguous() if False else xs
+                yd = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
+                t, lo, hi = timeit(lambda: fp8q.fp8_block_gemm(xd, sd, wq, ws, out=yd), args.iters, flush)
+                by = n * k + m * k + 4 * (m * k / 128 + n * k / 16384) + 2 * m * n
+                print(json.dumps({"kernel": "fp8_block_gemm_decode", "shape": [m, n, k], "ms": round(t, 4),
+                                  "GBps": round(by / (t * 1e-3) / 1e9, 1), "frac_hbm": round(by / (t * 1e-3) / 1e9 / HBM, 4)}))
+    if args.moe:
+        for T, skew in ((8192, 0.0), (8192, 1.2), (1024, 0.0)):
+            sizes = synth.moe_group_sizes(T, seed=0, skew=skew)
+            off = torch.from_numpy(synth.offsets_from_sizes(sizes)).to(dev)
+            rows = int(sizes.sum())
+            for name, (E, n, k) in synth.QWEN3_30B_EXPERTS.items():
+                w = (torch.randn((E * n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+                wq, ws = fp8q.quantize_weight_blockwise(w)
+                wq = wq.view(E, n, k)
+                ws = ws.view(E, n // 128, k // 128)
+                x = torch.randn((rows, k), generator=g, device=dev).to(torch.bfloat16)
+                xq, xs = fp8q.quantize_act_per_token_group(x)
+                y = torch.empty((rows, n), dtype=torch.bfloat16, device=dev)
+                t, lo, hi = timeit(lambda: fp8q.fp8_block_gemm_grouped(xq, xs, wq, ws, off, out=y), args.iters, flush)
+                tf = 2 * rows * n * k / (t * 1e-3) / 1e12
+                by = E * n * k + rows * k + 2 * rows * n
+                print(json.dumps({"kernel": "fp8_block_gemm_grouped", "T": T, "skew": skew, "name": name,
+                                  "shape": [rows, n, k, E], "ms": round(t, 4), "TFLOPs": round(tf, 1),
+                                  "frac_fp8": round(tf / FP8, 4), "GBps": round(by / (t * 1e-3) / 1e9, 1)}))
+
+
+if __name__ == "__main__":
+    main()
