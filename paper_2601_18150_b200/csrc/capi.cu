@@ -53,6 +53,8 @@ int32_t fp8q_version(void) { return 10000; }
 
 int64_t fp8q_kernel_launches(void) { return g_launches.load(); }
 
+void fp8q_debug_set_gemm_trace(uint32_t* dev_ptr) { fp8q::set_gemm_trace(dev_ptr); }
+
 fp8q_status quantize_weight_blockwise(const void* w_bf16, int64_t n, int64_t k, int64_t ld_w,
                                       uint8_t* codes, int64_t ld_q, float* scales, int64_t ld_s,
                                       int32_t* nonfinite_flag, void* stream) {

@@ -9,8 +9,8 @@
 //
 // CTA = 12 warps (3 warpgroups), persistent over 128x256 output tiles (M-fastest order so
 // concurrent CTAs share B tiles and the whole A panel stays L2-resident).  Warpgroup 0 gives
-// registers away (setmaxnreg.dec 56) and warpgroups 1-2 take them (setmaxnreg.inc 224): the
-// register file is per SM sub-partition, so 3 warps x 168 at launch become 56 + 224 + 224.
+// registers away (setmaxnreg.dec 72) and warpgroups 1-2 take them (setmaxnreg.inc 216): the
+// register file is per SM sub-partition, so 3 warps x 168 at launch become 72 + 216 + 216 (the CTA pool: 128 x 96 released = 256 x 48 taken).
 //   warp 0        TMA producer: per k-block, A 128x128 B and B 256x128 B into a 4-stage ring
 //                 (128-byte swizzle), mbarrier full/empty handshake with the MMA warp.
 //   warp 1        TMEM owner (512 columns) and MMA issuer: 4 x tcgen05.mma.kind::f8f6f4
@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "ptx.cuh"
@@ -38,19 +39,41 @@ namespace fp8q {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BN = 256;
 constexpr int BK = 128;
-constexpr int STAGES = 4;
 constexpr int A_TILE = BM * BK;  // bytes (E4M3)
-constexpr int B_TILE = BN * BK;
-constexpr int STAGE_BYTES = A_TILE + B_TILE;
 constexpr int NUM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
-constexpr int TMEM_COLS = 512;  // 2 partial buffers x 256 fp32 columns
+constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int RASTER_GM = 16;  // m-tiles per raster band
-constexpr uint32_t IDESC = idesc_e4m3_f32(BM, BN);
-constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
+constexpr int SMEM_BUDGET = 160 * 1024;  // operand stages
+// Output staging for the TMA-store epilogue: per promotion warp four 32-row x 64-byte
+// chunks (2 KB each, 64-byte swizzle) -> 8 warps x 8 KB.  A BF16 half-tile row segment
+// (128 columns) is exactly 4 chunks, so a tile's stores never wait for each other.
+constexpr int EPI_CHUNKS = 4;
+constexpr int EPI_CHUNK_BYTES = 32 * 64;
+constexpr int EPI_STAGE_BYTES = NUM_EPI_WARPS * EPI_CHUNKS * EPI_CHUNK_BYTES;
+// setmaxnreg budget: the CTA's register pool is fixed at launch (384 threads x 168), so what
+// warpgroup 0 releases must cover what warpgroups 1-2 take, or setmaxnreg.inc never returns.
+constexpr int REGS_LAUNCH = 168;
+constexpr int REGS_CTRL = 72;
+constexpr int REGS_EPI = 216;
+static_assert(128 * (REGS_LAUNCH - REGS_CTRL) >= 256 * (REGS_EPI - REGS_LAUNCH), "register pool overdrawn");
+
+// Tile configuration.  BN = 256: 2 TMEM partial buffers, 4 smem stages, 128 accumulator
+// registers per promotion thread.  BN = 128: 4 TMEM partial buffers (the tensor core can run
+// 3 k-blocks ahead of the promotion warps), 6 smem stages, 64 accumulators per thread.
+template <int BN_>
+struct Cfg {
+    static constexpr int BN = BN_;
+    static constexpr int B_TILE = BN * BK;
+    static constexpr int STAGE_BYTES = A_TILE + B_TILE;
+    static constexpr int STAGES = SMEM_BUDGET / STAGE_BYTES;
+    static constexpr int TMEM_BUFS = TMEM_COLS / BN;
+    static constexpr int EPI_COLS = BN / 2;  // columns per promotion thread
+    static constexpr uint32_t IDESC = idesc_e4m3_f32(BM, BN);
+    static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + EPI_STAGE_BYTES + 512;
+};
 
 struct KParams {
     const float* sa;
@@ -66,10 +89,23 @@ struct KParams {
     int num_kb;
     int num_n_tiles;
     const int32_t* offsets;  // nullptr: one group of m rows
+    uint32_t* trace;         // dev-only timeline (fp8q_debug_set_trace), nullptr in production
+    int debug_mode;          // dev-only: 1 = promotion skips TMEM loads + FMAs (MMA pipe ceiling),
+                             // 2 = also no TMA after the first stages (tensor-core-only ceiling)
     int groups;
 };
 
-// Walks the (group, m-tile, n-tile) sequence; t must increase between calls.
+// Dev-only timeline: CTA 0 records clock() at pipeline events of its first TRACE_KB k-blocks.
+constexpr int TRACE_KB = 96;
+constexpr int TRACE_EV = 8;
+__device__ __forceinline__ void trace_ev(const KParams& p, uint32_t it, int ev) {
+    if (p.trace != nullptr && blockIdx.x == 0 && it < TRACE_KB)
+        p.trace[it * TRACE_EV + ev] = static_cast<uint32_t>(clock64());
+}
+
+// Walks the (group, m-tile, n-tile) sequence; t must increase between calls.  TM = rows per
+// tile (128 for one CTA, 256 for a CTA pair), GM = m-tiles per raster band.
+template <int TM, int GM>
 struct TileCursor {
     int g;
     int64_t base;   // first linear tile index of group g
@@ -84,7 +120,7 @@ struct TileCursor {
             row0 = 0;
             rows = p.m;
         }
-        mtiles = (rows + BM - 1) / BM;
+        mtiles = (rows + TM - 1) / TM;
     }
     __device__ void init(const KParams& p) {
         g = 0;
@@ -99,14 +135,14 @@ struct TileCursor {
             if (++g >= p.groups) return false;
             load(p);
         }
-        // Grouped raster: bands of RASTER_GM m-tiles; inside a band m is fastest, so the ~148
+        // Grouped raster: bands of GM m-tiles; inside a band m is fastest, so the ~148
         // concurrent tiles cover a compact RASTER_GM x ~9 block of the output and both the A
         // band and the B tiles they touch stay L2-resident (K = 12288 would otherwise re-read A).
         const int64_t l = t - base;
-        const int64_t band = l / (int64_t(RASTER_GM) * p.num_n_tiles);
-        const int64_t r = l - band * (int64_t(RASTER_GM) * p.num_n_tiles);
-        const int64_t gm = min(int64_t(RASTER_GM), mtiles - band * RASTER_GM);
-        mt = static_cast<int>(band * RASTER_GM + r % gm);
+        const int64_t band = l / (int64_t(GM) * p.num_n_tiles);
+        const int64_t r = l - band * (int64_t(GM) * p.num_n_tiles);
+        const int64_t gm = min(int64_t(GM), mtiles - band * GM);
+        mt = static_cast<int>(band * GM + r % gm);
         nt = static_cast<int>(r / gm);
         return true;
     }
@@ -121,19 +157,227 @@ __device__ __forceinline__ void ffma2(float2& acc, const float2 v, const float f
     acc = *reinterpret_cast<float2*>(&a);
 }
 
+// One output tile's promotion + store, for one promotion thread: its row `row`, columns
+// [col0, col0 + EPI_COLS).  For every k-block: wait for the partial in TMEM buffer it % NBUF,
+// tcgen05.ld it, hand the buffer back (to the leader CTA of a pair when PAIR), and
+// acc += P_kb * (sa[kb][row] * sb[col0/128][kb]) with packed FFMA2.
+// One promotion thread's share of an output tile: row `row`, columns [col0, col0 + BN/2).
+struct EpiTile {
+    int64_t row;      // this thread's output row
+    int64_t row_end;  // end of the rows this tile may write (group end / m)
+    int64_t col0;     // first of this thread's columns
+    int g;            // group (MoE expert) index
+};
+// The first two k-blocks' (sa, sb) of a tile: loaded one tile ahead so the HBM/L2 latency of
+// the first scales overlaps the previous tile's last k-blocks and stores.
+struct ScalePre {
+    float sa0, sb0, sa1, sb1;
+};
+__device__ __forceinline__ bool tile_live(const KParams& p, const EpiTile& t) {
+    return t.row < t.row_end && t.col0 < p.n;
+}
+__device__ __forceinline__ ScalePre prefetch_scales(const KParams& p, const EpiTile& t) {
+    ScalePre s{0.f, 0.f, 0.f, 0.f};
+    if (tile_live(p, t)) {
+        const float* sap = p.sa + t.row;
+        const float* sbp = p.sb + int64_t(t.g) * p.stride_sb + (t.col0 / 128) * p.ld_sb;
+        s.sa0 = __ldg(sap);
+        s.sb0 = __ldg(sbp);
+        if (p.num_kb > 1) {
+            s.sa1 = __ldg(sap + p.ld_sa);
+            s.sb1 = __ldg(sbp + 1);
+        }
+    }
+    return s;
+}
+
+// For every k-block: wait for the partial in TMEM buffer it % NBUF, tcgen05.ld it, hand the
+// buffer back (to the leader CTA of a pair when PAIR), and
+// acc += P_kb * (sa[kb][row] * sb[col0/128][kb]) with packed FFMA2; then store the tile.
+template <int BN, int NBUF, bool PAIR>
+__device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap* tmD, uint8_t* stg,
+                                             const EpiTile& tile, const ScalePre& pre, bool has_next,
+                                             const EpiTile& next, ScalePre& next_pre, uint32_t tmem,
+                                             int qd, int h, int lane, uint64_t* tfull,
+                                             uint64_t* tempty, uint32_t& it) {
+    constexpr int EPI_COLS = BN / 2;
+    constexpr int CHUNKS = EPI_COLS / 32;  // tcgen05.ld 32x32b.x32 per promotion thread
+    static_assert(EPI_COLS / 32 <= EPI_CHUNKS, "BF16 row segment must fit the staging chunks");
+    const int64_t row = tile.row;
+    const int64_t row_end = tile.row_end;
+    const int64_t col0 = tile.col0;
+    const bool live = tile_live(p, tile);
+    const float* sap = p.sa + row;
+    const float* sbp = p.sb + int64_t(tile.g) * p.stride_sb + (col0 / 128) * p.ld_sb;
+    float2 acc[EPI_COLS / 2];
+#pragma unroll
+    for (int j = 0; j < EPI_COLS / 2; ++j) acc[j] = make_float2(0.f, 0.f);
+    // Scale prefetch two k-blocks ahead; the raw values are only multiplied when used,
+    // so the load latency never sits between the TMEM-full wait and the FMAs.
+    float sa0 = pre.sa0, sb0 = pre.sb0, sa1 = pre.sa1, sb1 = pre.sb1;
+    for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+        const float f = sa0 * sb0;
+        sa0 = sa1;
+        sb0 = sb1;
+        if (live && kb + 2 < p.num_kb) {
+            sa1 = __ldg(sap + int64_t(kb + 2) * p.ld_sa);
+            sb1 = __ldg(sbp + kb + 2);
+        }
+        if (has_next && kb == (p.num_kb > 4 ? p.num_kb - 4 : 0)) next_pre = prefetch_scales(p, next);
+        const uint32_t buf = it % NBUF;
+        const uint32_t bph = (it / NBUF) & 1u;
+        mbar_wait(&tfull[buf], bph);
+        tc_fence_after();
+        const bool tr = (threadIdx.x == EPI_WARP0 * 32);
+        if (tr) trace_ev(p, it, 3);
+        if (p.debug_mode >= 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (PAIR)
+                    mbar_arrive_cluster(&tempty[buf], 0);
+                else
+                    mbar_arrive(&tempty[buf]);
+            }
+            continue;
+        }
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * BN + h * EPI_COLS;
+        // Software-pipelined: the tcgen05.ld of chunk c+1 is in flight while chunk c's FMAs
+        // issue, so each TMEM load latency after the first overlaps useful work.
+        float v[2][32];
+        tmem_ld_32x32b_x32(taddr, v[0]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < CHUNKS; ++c) {
+            if (c + 1 < CHUNKS) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                ffma2(acc[c * 16 + j], make_float2(v[c & 1][2 * j], v[c & 1][2 * j + 1]), f);
+            if (c + 1 < CHUNKS) tmem_wait_ld();
+            if (c + 2 == CHUNKS || CHUNKS == 1) {  // last chunk loaded: hand the buffer back
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (tr) trace_ev(p, it, 4);
+                    if (PAIR)
+                        mbar_arrive_cluster(&tempty[buf], 0);
+                    else
+                        mbar_arrive(&tempty[buf]);
+                }
+            }
+        }
+        if (tr) trace_ev(p, it, 5);
+    }
+    const bool tr_store = (threadIdx.x == EPI_WARP0 * 32);
+    if (tr_store) trace_ev(p, it - 1, 6);
+    if (col0 >= p.n) return;  // warp-uniform: these columns are past the matrix
+    // ---- output: the warp's 32 rows x EPI_COLS columns.  Full 32-row slices go through
+    // swizzled smem chunks (32 rows x 64 B) and asynchronous TMA stores (the tensor map clips
+    // at m and n); a slice that straddles the end of a MoE group (rows past it belong to the
+    // next group) is written with masked direct stores instead.
+    const int64_t row_base = row - lane;
+    if (row_base + 32 <= row_end || p.offsets == nullptr) {
+        const uint32_t swz = static_cast<uint32_t>((lane >> 1) & 3);
+        if (p.out_f32) {
+#pragma unroll
+            for (int c = 0; c < EPI_COLS / 16; ++c) {
+                uint8_t* sb = stg + (c % EPI_CHUNKS) * EPI_CHUNK_BYTES;
+                if (lane == 0) bulk_wait_group_read<EPI_CHUNKS - 1>();
+                __syncwarp();
+                const uint32_t base = smem_u32(sb) + lane * 64;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float2 a0 = acc[c * 8 + j * 2], a1 = acc[c * 8 + j * 2 + 1];
+                    st_shared_v4(base + 16u * (static_cast<uint32_t>(j) ^ swz), __float_as_uint(a0.x),
+                                 __float_as_uint(a0.y), __float_as_uint(a1.x), __float_as_uint(a1.y));
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(tmD, sb, static_cast<int32_t>(col0 + c * 16), static_cast<int32_t>(row_base));
+                    bulk_commit_group();
+                }
+            }
+        } else {
+            // BF16: the thread's 128 columns are exactly EPI_CHUNKS chunks -> write them all,
+            // one async-proxy fence, then the chunk stores.
+            if (lane == 0) bulk_wait_group_read<0>();  // previous tile's stores left the chunks
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < EPI_COLS / 32; ++c) {
+                const uint32_t base = smem_u32(stg + c * EPI_CHUNK_BYTES) + lane * 64;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 a = acc[c * 16 + j * 4 + e];
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(a.x, a.y);
+                        w[e] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    st_shared_v4(base + 16u * (static_cast<uint32_t>(j) ^ swz), w[0], w[1], w[2], w[3]);
+                }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int c = 0; c < EPI_COLS / 32; ++c)
+                    tma_store_2d(tmD, stg + c * EPI_CHUNK_BYTES, static_cast<int32_t>(col0 + c * 32),
+                                 static_cast<int32_t>(row_base));
+                bulk_commit_group();
+            }
+        }
+        if (tr_store) trace_ev(p, it - 1, 7);
+        return;
+    }
+    if (!live) return;
+    if (p.out_f32) {
+        float* drow = static_cast<float*>(p.d) + row * p.ld_d + col0;
+#pragma unroll
+        for (int j = 0; j < EPI_COLS / 4; ++j) {
+            if (col0 + j * 4 < p.n)
+                st_v4(drow + j * 4, __float_as_uint(acc[2 * j].x), __float_as_uint(acc[2 * j].y),
+                      __float_as_uint(acc[2 * j + 1].x), __float_as_uint(acc[2 * j + 1].y));
+        }
+    } else {
+        __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.d) + row * p.ld_d + col0;
+#pragma unroll
+        for (int j = 0; j < EPI_COLS / 8; ++j) {
+            if (col0 + j * 8 < p.n) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[4 * j + e].x, acc[4 * j + e].y);
+                    w[e] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                st_v4(drow + j * 8, w[0], w[1], w[2], w[3]);
+            }
+        }
+    }
+}
+
+template <int BN_>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     fp8_block_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmB, const KParams p) {
+                          const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmD, const KParams p) {
+    using C = Cfg<BN_>;
+    constexpr int BN = C::BN;
+    constexpr int STAGES = C::STAGES;
+    constexpr int NBUF = C::TMEM_BUFS;
+    constexpr int EPI_COLS = C::EPI_COLS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* smA = smem;
     uint8_t* smB = smem + STAGES * A_TILE;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint8_t* smEpi = smem + STAGES * C::STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smEpi + EPI_STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -143,7 +387,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], NUM_EPI_WARPS);
         }
@@ -154,14 +398,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     tc_fence_after();
 
-    if (warp < EPI_WARP0) regs_dec<56>();
+    if (warp < EPI_WARP0) regs_dec<REGS_CTRL>();
 
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------------------ TMA producer
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
-            TileCursor cur;
+            TileCursor<BM, RASTER_GM> cur;
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
@@ -171,10 +415,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
+                    if (p.debug_mode == 2 && it >= STAGES) break;  // dev: operands stay resident
                     mbar_wait(&empty[stage], ph ^ 1u);
-                    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                    trace_ev(p, it, 0);
+                    mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
                     tma_load_2d(smA + stage * A_TILE, &tmA, &full[stage], kb * BK, arow);
-                    tma_load_3d(smB + stage * B_TILE, &tmB, &full[stage], kb * BK, brow, cur.g);
+                    tma_load_3d(smB + stage * C::B_TILE, &tmB, &full[stage], kb * BK, brow, cur.g);
                 }
             }
         }
@@ -182,7 +428,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) {
             // ------------------------------------------------------------ MMA issuer
             const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
-            TileCursor cur;
+            TileCursor<BM, RASTER_GM> cur;
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
@@ -190,18 +436,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
-                    const uint32_t buf = it & 1u;
-                    const uint32_t bph = (it >> 1) & 1u;
+                    const uint32_t buf = it % NBUF;
+                    const uint32_t bph = (it / NBUF) & 1u;
                     mbar_wait(&tempty[buf], bph ^ 1u);  // promotion warps drained this buffer
-                    mbar_wait(&full[stage], ph);        // TMA landed A and B
+                    trace_ev(p, it, 1);
+                    if (p.debug_mode != 2 || it < STAGES) mbar_wait(&full[stage], ph);  // TMA landed A and B
+                    trace_ev(p, it, 2);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(smA + stage * A_TILE);
-                    const uint32_t b0 = smem_u32(smB + stage * B_TILE);
+                    const uint32_t b0 = smem_u32(smB + stage * C::B_TILE);
                     const uint32_t d = tmem + buf * BN;
 #pragma unroll
                     for (int kk = 0; kk < BK / 32; ++kk)
                         mma_f8f6f4(d, smem_desc_k_sw128(a0 + kk * 32), smem_desc_k_sw128(b0 + kk * 32),
-                                   IDESC, kk > 0 ? 1u : 0u);
+                                   C::IDESC, kk > 0 ? 1u : 0u);
                     mma_commit(&empty[stage]);
                     mma_commit(&tfull[buf]);
                 }
@@ -209,97 +457,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp >= EPI_WARP0) {
         // ---------------------------------------------------------------- promotion warps
-        regs_inc<224>();
-        const int h = (warp - EPI_WARP0) >> 2;  // column half: n-block 2*nt + h
-        const int qd = warp & 3;         // TMEM lane quarter this warp may access
+        regs_inc<REGS_EPI>();
+        const int h = (warp - EPI_WARP0) >> 2;  // column half of the tile
+        const int qd = warp & 3;                // TMEM lane quarter this warp may access
         const int r_in_tile = qd * 32 + lane;
+        uint8_t* stg = smEpi + (warp - EPI_WARP0) * EPI_CHUNKS * EPI_CHUNK_BYTES;
         const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
-        float2 acc[64];
-        TileCursor cur;
+        TileCursor<BM, RASTER_GM> cur;
         cur.init(p);
         uint32_t it = 0;
-        int mt, nt;
-        for (int64_t t = blockIdx.x; cur.seek(p, t, mt, nt); t += gridDim.x) {
-            const int64_t rloc = int64_t(mt) * BM + r_in_tile;
-            const bool row_ok = rloc < cur.rows;
-            const int64_t row = cur.row0 + rloc;
-            const int64_t nb = int64_t(nt) * 2 + h;
-            const bool nb_ok = nb * 128 < p.n;
-            const bool live = row_ok && nb_ok;
-            const float* sap = p.sa + row;
-            const float* sbp = p.sb + int64_t(cur.g) * p.stride_sb + nb * p.ld_sb;
-#pragma unroll
-            for (int j = 0; j < 64; ++j) acc[j] = make_float2(0.f, 0.f);
-            // Scale prefetch two k-blocks ahead; the raw values are only multiplied when used,
-            // so the load latency never sits between the TMEM-full wait and the FMAs.
-            float sa0 = 0.f, sb0 = 0.f, sa1 = 0.f, sb1 = 0.f;
-            if (live) {
-                sa0 = __ldg(sap);
-                sb0 = __ldg(sbp);
-                if (p.num_kb > 1) {
-                    sa1 = __ldg(sap + p.ld_sa);
-                    sb1 = __ldg(sbp + 1);
-                }
-            }
-            for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-                const float f = sa0 * sb0;
-                sa0 = sa1;
-                sb0 = sb1;
-                if (live && kb + 2 < p.num_kb) {
-                    sa1 = __ldg(sap + int64_t(kb + 2) * p.ld_sa);
-                    sb1 = __ldg(sbp + kb + 2);
-                }
-                const uint32_t buf = it & 1u;
-                const uint32_t bph = (it >> 1) & 1u;
-                mbar_wait(&tfull[buf], bph);
-                tc_fence_after();
-                const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * BN + h * 128;
-#pragma unroll
-                for (int c = 0; c < 4; c += 2) {
-                    float v0[32], v1[32];
-                    tmem_ld_32x32b_x32(taddr + c * 32, v0);
-                    tmem_ld_32x32b_x32(taddr + (c + 1) * 32, v1);
-                    tmem_wait_ld();
-                    if (c == 2) {  // whole partial read: hand the buffer back to the MMA warp
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[buf]);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        ffma2(acc[c * 16 + j], make_float2(v0[2 * j], v0[2 * j + 1]), f);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        ffma2(acc[(c + 1) * 16 + j], make_float2(v1[2 * j], v1[2 * j + 1]), f);
-                }
-            }
-            if (live) {
-                const int64_t col0 = nb * 128;
-                if (p.out_f32) {
-                    float* drow = static_cast<float*>(p.d) + row * p.ld_d + col0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (col0 + j * 4 < p.n)
-                            st_v4(drow + j * 4, __float_as_uint(acc[2 * j].x), __float_as_uint(acc[2 * j].y),
-                                  __float_as_uint(acc[2 * j + 1].x), __float_as_uint(acc[2 * j + 1].y));
-                    }
-                } else {
-                    __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.d) + row * p.ld_d + col0;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        if (col0 + j * 8 < p.n) {
-                            uint32_t w[4];
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[4 * j + e].x, acc[4 * j + e].y);
-                                w[e] = *reinterpret_cast<uint32_t*>(&b2);
-                            }
-                            st_v4(drow + j * 8, w[0], w[1], w[2], w[3]);
-                        }
-                    }
-                }
-            }
+        auto make_tile = [&](int mt, int nt) {
+            return EpiTile{cur.row0 + int64_t(mt) * BM + r_in_tile, cur.row0 + cur.rows,
+                           int64_t(nt) * BN + h * EPI_COLS, cur.g};
+        };
+        int mt = 0, nt = 0;
+        int64_t t = blockIdx.x;
+        bool have = cur.seek(p, t, mt, nt);
+        EpiTile tile = have ? make_tile(mt, nt) : EpiTile{0, 0, 0, 0};
+        ScalePre pre = prefetch_scales(p, tile);
+        while (have) {
+            const int64_t tn = t + gridDim.x;
+            const bool have_next = cur.seek(p, tn, mt, nt);
+            const EpiTile next = have_next ? make_tile(mt, nt) : tile;
+            ScalePre next_pre = pre;
+            promote_tile<BN, NBUF, false>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd, h,
+                                          lane, tfull, tempty, it);
+            tile = next;
+            pre = next_pre;
+            t = tn;
+            have = have_next;
         }
+        if (lane == 0) bulk_wait_group<0>();
     }
 
     tc_fence_before();
@@ -307,6 +495,184 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(*reinterpret_cast<volatile uint32_t*>(tmem_slot), TMEM_COLS);
+    }
+}
+
+// ------------------------------------------------------------------------------ CTA pair
+// cta_group::2: a cluster of 2 CTAs on 2 SMs computes a 256 x 256 output tile.  CTA r loads A
+// rows [m0 + 128r, +128) and B rows [n0 + 128r, +128) into its own smem; the leader's single
+// MMA thread issues M=256, N=256 tcgen05.mma that reads A from each CTA's smem for that CTA's
+// rows and B from both CTAs' smem, and writes each CTA's 128 rows x 256 fp32 into that CTA's
+// TMEM.  Per SM and k-block this moves 32 KB from L2 instead of 48 KB (1-CTA 128x256), the
+// operand-traffic ceiling that limited the 1-CTA kernel.  Barriers: full[s] lives in the
+// leader (both CTAs' TMA bytes + the peer's arrival land there); empty[s] and tfull[b] are
+// arrived in both CTAs by a multicast tcgen05.commit; tempty[b] lives in the leader and
+// collects the 16 promotion warps of the pair.
+template <int PBN>
+struct PairCfg {
+    static constexpr int BN = PBN;          // MMA N (tile columns)
+    static constexpr int B_HALF = PBN / 2;  // B rows loaded by each CTA
+    static constexpr int STAGE_BYTES = A_TILE + B_HALF * BK;  // per CTA
+    static constexpr int STAGES = SMEM_BUDGET / STAGE_BYTES;
+    static constexpr int NBUF = TMEM_COLS / PBN;
+    static constexpr uint32_t IDESC = idesc_e4m3_f32(2 * BM, PBN);
+    static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + EPI_STAGE_BYTES + 512;
+};
+constexpr int PAIR_RASTER_GM = 8;  // pair m-tiles (256 rows) per raster band
+
+template <int PBN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    fp8_block_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                               const __grid_constant__ CUtensorMap tmB,
+                               const __grid_constant__ CUtensorMap tmD, const KParams p) {
+    using PC = PairCfg<PBN>;
+    constexpr int STAGES = PC::STAGES;
+    constexpr int NBUF = PC::NBUF;
+    constexpr int PAIR_BN = PC::BN;
+    constexpr int PAIR_B_HALF = PC::B_HALF;
+    constexpr int PAIR_STAGE_BYTES = PC::STAGE_BYTES;
+    constexpr uint32_t PAIR_IDESC = PC::IDESC;
+    constexpr int EPI_COLS = PAIR_BN / 2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smA = smem;
+    uint8_t* smB = smem + STAGES * A_TILE;
+    uint8_t* smEpi = smem + STAGES * PAIR_STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smEpi + EPI_STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int64_t pair = blockIdx.x >> 1;
+    const int64_t npairs = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 2);   // leader: own arrive.expect_tx + the peer's arrive
+            mbar_init(&empty[s], 1);  // multicast commit
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);                  // multicast commit
+            mbar_init(&tempty[b], 2 * NUM_EPI_WARPS);  // leader: promotion warps of both CTAs
+        }
+        fence_mbar_init();
+    }
+    cluster_sync_all();
+    if (warp == 1) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+
+    if (warp < EPI_WARP0) regs_dec<REGS_CTRL>();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ TMA producer (both CTAs)
+            tma_prefetch_desc(&tmA);
+            tma_prefetch_desc(&tmB);
+            TileCursor<2 * BM, PAIR_RASTER_GM> cur;
+            cur.init(p);
+            uint32_t it = 0;
+            int mt, nt;
+            for (int64_t t = pair; cur.seek(p, t, mt, nt); t += npairs) {
+                const int32_t arow = static_cast<int32_t>(cur.row0 + int64_t(mt) * 2 * BM + rank * BM);
+                const int32_t brow = nt * PAIR_BN + static_cast<int32_t>(rank) * PAIR_B_HALF;
+                for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+                    const uint32_t stage = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1u;
+                    mbar_wait(&empty[stage], ph ^ 1u);
+                    trace_ev(p, it, 0);
+                    if (leader)
+                        mbar_arrive_expect_tx(&full[stage], 2 * PAIR_STAGE_BYTES);
+                    else
+                        mbar_arrive_cluster(&full[stage], 0);
+                    tma_load_2d_pair(smA + stage * A_TILE, &tmA, &full[stage], kb * BK, arow);
+                    tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK), &tmB, &full[stage], kb * BK, brow, cur.g);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            // ------------------------------------------------------------ MMA issuer (leader)
+            const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+            TileCursor<2 * BM, PAIR_RASTER_GM> cur;
+            cur.init(p);
+            uint32_t it = 0;
+            int mt, nt;
+            for (int64_t t = pair; cur.seek(p, t, mt, nt); t += npairs) {
+                for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+                    const uint32_t stage = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1u;
+                    const uint32_t buf = it % NBUF;
+                    const uint32_t bph = (it / NBUF) & 1u;
+                    mbar_wait(&tempty[buf], bph ^ 1u);
+                    trace_ev(p, it, 1);
+                    mbar_wait(&full[stage], ph);
+                    trace_ev(p, it, 2);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smA + stage * A_TILE);
+                    const uint32_t b0 = smem_u32(smB + stage * (PAIR_B_HALF * BK));
+                    const uint32_t d = tmem + buf * PAIR_BN;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 32; ++kk)
+                        mma_f8f6f4_pair(d, smem_desc_k_sw128(a0 + kk * 32), smem_desc_k_sw128(b0 + kk * 32),
+                                        PAIR_IDESC, kk > 0 ? 1u : 0u);
+                    mma_commit_pair(&empty[stage], 0x3);
+                    mma_commit_pair(&tfull[buf], 0x3);
+                }
+            }
+            // the peer's last remote arrivals must land before the barriers go away
+            for (uint32_t j = 0; j < NBUF && j < it; ++j) {
+                const uint32_t i = it - 1 - j;
+                mbar_wait(&tempty[i % NBUF], (i / NBUF) & 1u);
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ---------------------------------------------------------------- promotion warps
+        regs_inc<REGS_EPI>();
+        const int h = (warp - EPI_WARP0) >> 2;
+        const int qd = warp & 3;
+        const int r_in_tile = qd * 32 + lane;
+        uint8_t* stg = smEpi + (warp - EPI_WARP0) * EPI_CHUNKS * EPI_CHUNK_BYTES;
+        const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+        TileCursor<2 * BM, PAIR_RASTER_GM> cur;
+        cur.init(p);
+        uint32_t it = 0;
+        auto make_tile = [&](int mt, int nt) {
+            return EpiTile{cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM + r_in_tile,
+                           cur.row0 + cur.rows, int64_t(nt) * PAIR_BN + h * EPI_COLS, cur.g};
+        };
+        int mt = 0, nt = 0;
+        int64_t t = pair;
+        bool have = cur.seek(p, t, mt, nt);
+        EpiTile tile = have ? make_tile(mt, nt) : EpiTile{0, 0, 0, 0};
+        ScalePre pre = prefetch_scales(p, tile);
+        while (have) {
+            const int64_t tn = t + npairs;
+            const bool have_next = cur.seek(p, tn, mt, nt);
+            const EpiTile next = have_next ? make_tile(mt, nt) : tile;
+            ScalePre next_pre = pre;
+            promote_tile<PAIR_BN, NBUF, true>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd,
+                                              h, lane, tfull, tempty, it);
+            tile = next;
+            pre = next_pre;
+            t = tn;
+            have = have_next;
+        }
+        if (lane == 0) bulk_wait_group<0>();
+    }
+
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair(*reinterpret_cast<volatile uint32_t*>(tmem_slot), TMEM_COLS);
     }
 }
 
@@ -325,6 +691,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
+uint32_t* g_trace = nullptr;
+
 struct DeviceInfo {
     int sms = 0;
     bool attr_set = false;
@@ -342,8 +710,17 @@ cudaError_t device_info(int& sms) {
     if (!di.attr_set) {
         e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(fp8_block_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(SMEM_BYTES));
+        e = cudaFuncSetAttribute(fp8_block_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(Cfg<128>::SMEM_BYTES));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(fp8_block_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(Cfg<256>::SMEM_BYTES));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(fp8_block_gemm_pair_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(PairCfg<256>::SMEM_BYTES));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(fp8_block_gemm_pair_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(PairCfg<128>::SMEM_BYTES));
         if (e != cudaSuccess) return e;
         di.attr_set = true;
     }
@@ -351,17 +728,25 @@ cudaError_t device_info(int& sms) {
     return cudaSuccess;
 }
 
-}  // namespace
+// Kernel choice (see launch_cfg): env FP8Q_GEMM_KIND = 128 | 256 | 1128 | 1256 overrides (dev only).
+// Default: the CTA-pair kernel, except for M < 256 where one CTA per 128 x 256 tile wastes less.
+int choose_kind(const GemmArgs& a) {
+    static int forced = [] {
+        const char* e = std::getenv("FP8Q_GEMM_KIND");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 128 || forced == 256 || forced == 1128 || forced == 1256) return forced;
+    if (a.offsets == nullptr && a.m < 2 * BM) return 256;
+    return 1256;
+}
 
-cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* launches) {
-    *launches = 0;
-    if (a.m == 0 || a.n == 0 || a.groups == 0) return cudaSuccess;
-    auto encode = tensor_map_encoder();
-    if (encode == nullptr) return cudaErrorNotSupported;
-    int sms = 0;
-    cudaError_t e = device_info(sms);
-    if (e != cudaSuccess) return e;
-
+// kind: 128 / 256 = one-CTA kernel with that BN; 1128 / 1256 = CTA-pair kernel, 256 x BN tiles.
+template <int KIND>
+cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encode, int sms,
+                       cudaStream_t stream) {
+    constexpr bool kPair = KIND > 1000;
+    constexpr int BN = kPair ? KIND - 1000 : KIND;
+    constexpr int B_BOX = kPair ? BN / 2 : KIND;
     CUtensorMap tmA, tmB;
     {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.m)};
@@ -380,7 +765,7 @@ cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* l
         cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.n),
                               static_cast<cuuint64_t>(g)};
         cuuint64_t strides[2] = {static_cast<cuuint64_t>(a.ld_b), static_cast<cuuint64_t>(sb)};
-        cuuint32_t box[3] = {BK, BN, 1};
+        cuuint32_t box[3] = {BK, static_cast<cuuint32_t>(B_BOX), 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(a.b), dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -388,8 +773,26 @@ cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* l
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
-
+    CUtensorMap tmD;
+    {
+        const int esz = a.out_f32 ? 4 : 2;
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.n), static_cast<cuuint64_t>(a.m)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_d * esz)};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(64 / esz), 32};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = encode(&tmD, a.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                            2, a.d, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
     KParams p;
+    p.trace = g_trace;
+    static const int debug_mode = [] {
+        const char* e = std::getenv("FP8Q_GEMM_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.debug_mode = debug_mode;
     p.sa = a.sa;
     p.ld_sa = a.ld_sa;
     p.sb = a.sb;
@@ -405,14 +808,46 @@ cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* l
     p.offsets = a.offsets;
     p.groups = a.offsets != nullptr ? a.groups : 1;
 
-    int64_t grid = sms;
-    if (a.offsets == nullptr) {
-        const int64_t tiles = ((a.m + BM - 1) / BM) * p.num_n_tiles;
-        grid = tiles < sms ? tiles : sms;
+    if (kPair) {
+        int64_t clusters = sms / 2;
+        if (a.offsets == nullptr) {
+            const int64_t tiles = ((a.m + 2 * BM - 1) / (2 * BM)) * p.num_n_tiles;
+            clusters = tiles < clusters ? tiles : clusters;
+        }
+        fp8_block_gemm_pair_kernel<BN><<<static_cast<unsigned>(2 * clusters), NUM_THREADS,
+                                         PairCfg<BN>::SMEM_BYTES, stream>>>(tmA, tmB, tmD, p);
+    } else {
+        int64_t grid = sms;
+        if (a.offsets == nullptr) {
+            const int64_t tiles = ((a.m + BM - 1) / BM) * p.num_n_tiles;
+            grid = tiles < sms ? tiles : sms;
+        }
+        fp8_block_gemm_kernel<BN><<<static_cast<unsigned>(grid), NUM_THREADS, Cfg<BN>::SMEM_BYTES, stream>>>(
+            tmA, tmB, tmD, p);
     }
-    fp8_block_gemm_kernel<<<static_cast<unsigned>(grid), NUM_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
-    *launches = 1;
     return cudaGetLastError();
+}
+
+}  // namespace
+
+void set_gemm_trace(uint32_t* dev_ptr) { g_trace = dev_ptr; }
+
+cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* launches) {
+    *launches = 0;
+    if (a.m == 0 || a.n == 0 || a.groups == 0) return cudaSuccess;
+    auto encode = tensor_map_encoder();
+    if (encode == nullptr) return cudaErrorNotSupported;
+    int sms = 0;
+    cudaError_t e = device_info(sms);
+    if (e != cudaSuccess) return e;
+    switch (choose_kind(a)) {
+        case 128: e = launch_cfg<128>(a, encode, sms, stream); break;
+        case 256: e = launch_cfg<256>(a, encode, sms, stream); break;
+        case 1128: e = launch_cfg<1128>(a, encode, sms, stream); break;
+        default: e = launch_cfg<1256>(a, encode, sms, stream); break;
+    }
+    if (e == cudaSuccess) *launches = 1;
+    return e;
 }
 
 }  // namespace fp8q

@@ -1,0 +1,50 @@
+#!/usr/bin/env python3
+"""Launch one kernel shape a few times (target for `ncu -k regex:... -s W -c N`).
+usage: one_gemm.py gemm M N K | wq N K | aq M K | grouped T name [skew]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2601_18150_b200 import fp8q  # noqa: E402
+
+what = sys.argv[1]
+reps = int(os.environ.get("REPS", "5"))
+dev = torch.device("cuda")
+g = torch.Generator(device=dev)
+g.manual_seed(0)
+if what == "gemm":
+    m, n, k = map(int, sys.argv[2:5])
+    w = (torch.randn((n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    x = torch.randn((m, k), generator=g, device=dev).to(torch.bfloat16)
+    wq, ws = fp8q.quantize_weight_blockwise(w)
+    xq, xs = fp8q.quantize_act_per_token_group(x)
+    y = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
+    for _ in range(reps):
+        fp8q.fp8_block_gemm(xq, xs, wq, ws, out=y)
+elif what == "wq":
+    n, k = map(int, sys.argv[2:4])
+    w = (torch.randn((n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    for _ in range(reps):
+        fp8q.quantize_weight_blockwise(w)
+elif what == "aq":
+    m, k = map(int, sys.argv[2:4])
+    x = torch.randn((m, k), generator=g, device=dev).to(torch.bfloat16)
+    for _ in range(reps):
+        fp8q.quantize_act_per_token_group(x)
+elif what == "grouped":
+    T = int(sys.argv[2])
+    E, n, k = synth.QWEN3_30B_EXPERTS[sys.argv[3]]
+    skew = float(sys.argv[4]) if len(sys.argv) > 4 else 0.0
+    sizes = synth.moe_group_sizes(T, seed=0, skew=skew)
+    off = torch.from_numpy(synth.offsets_from_sizes(sizes)).to(dev)
+    rows = int(sizes.sum())
+    w = (torch.randn((E * n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    wq, ws = fp8q.quantize_weight_blockwise(w)
+    x = torch.randn((rows, k), generator=g, device=dev).to(torch.bfloat16)
+    xq, xs = fp8q.quantize_act_per_token_group(x)
+    for _ in range(reps):
+        fp8q.fp8_block_gemm_grouped(xq, xs, wq.view(E, n, k), ws.view(E, n // 128, k // 128), off)
+torch.cuda.synchronize()
