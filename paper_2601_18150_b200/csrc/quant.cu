@@ -178,6 +178,247 @@ __global__ void __launch_bounds__(256) act_per_token_group_kernel(
     }
 }
 
+// =======================================================================================
+// Wide-vector persistent variants (the production path when alignment allows).
+//   * 32-byte loads (LDG.256: 16 BF16 per thread per load) and 16-byte code stores;
+//   * packed f32x2 Markstein quotient (FMUL2/FFMA2: half the instructions per element);
+//   * the sign of zero is restored by OR-ing each input's sign bit into its code byte
+//     (a no-op for every nonzero input, and exactly IEEE's -0 / s = -0 for x = -0);
+//   * persistent CTAs/warps that issue the NEXT block's loads before encoding the current
+//     one, so every SM keeps a full block of HBM reads in flight.
+// =======================================================================================
+__device__ __forceinline__ void ld_v8(const void* p, uint32_t (&r)[8]) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st_v4_na(void* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t abs_max_bits16(const uint32_t (&w)[8]) {
+    const uint32_t m = 0x7FFF7FFFu;
+    uint32_t a = __vmaxu2(__vmaxu2(__vmaxu2(w[0] & m, w[1] & m), __vmaxu2(w[2] & m, w[3] & m)),
+                          __vmaxu2(__vmaxu2(w[4] & m, w[5] & m), __vmaxu2(w[6] & m, w[7] & m)));
+    return max(a & 0xFFFFu, a >> 16);
+}
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+    return (static_cast<uint64_t>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ float lo_of(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float hi_of(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+// (x0, x1) -> (RN32(x0 / s), RN32(x1 / s)) for blocks with amax >= 2^-104 (see header);
+// rr = (r, r), nss = (-s, -s).  The sign of a zero quotient is fixed later (sign OR).
+__device__ __forceinline__ uint64_t quot2_fast(uint64_t x, uint64_t rr, uint64_t nss) {
+    uint64_t q0, e, q1;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(q0) : "l"(x), "l"(rr));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(q0), "l"(nss), "l"(x));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(q1) : "l"(e), "l"(rr), "l"(q0));
+    return q1;
+}
+// 16 BF16 (8 words) -> 16 E4M3 codes (4 words).
+template <bool kFast>
+__device__ __forceinline__ uint4 encode16(const uint32_t (&w)[8], float s, float r) {
+    const uint64_t rr = pack2(r, r);
+    const uint64_t nss = pack2(-s, -s);
+    uint32_t c[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
+        float q0, q1, q2, q3;
+        if (kFast) {
+            const uint64_t qa = quot2_fast(pack2(__uint_as_float(wa << 16), __uint_as_float(wa & 0xFFFF0000u)), rr, nss);
+            const uint64_t qb = quot2_fast(pack2(__uint_as_float(wb << 16), __uint_as_float(wb & 0xFFFF0000u)), rr, nss);
+            q0 = lo_of(qa);
+            q1 = hi_of(qa);
+            q2 = lo_of(qb);
+            q3 = hi_of(qb);
+        } else {
+            q0 = __fdiv_rn(__uint_as_float(wa << 16), s);
+            q1 = __fdiv_rn(__uint_as_float(wa & 0xFFFF0000u), s);
+            q2 = __fdiv_rn(__uint_as_float(wb << 16), s);
+            q3 = __fdiv_rn(__uint_as_float(wb & 0xFFFF0000u), s);
+        }
+        const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;  // input sign bits
+        c[i] = (cvt_e4m3x2(q0, q1) | (cvt_e4m3x2(q2, q3) << 16)) | sign;
+    }
+    return make_uint4(c[0], c[1], c[2], c[3]);
+}
+
+// ---------------------------------------------------------------------------------------
+// Weights, wide path: requires k % 16 == 0, w 32-byte aligned with ld_w % 16 == 0, codes
+// 16-byte aligned with ld_q % 16 == 0.  CTA = 256 threads handles whole 128x128 blocks,
+// blk = blockIdx.x, += gridDim.x.  Thread (warp w, lane l) owns rows 16w + 4i + (l >> 3),
+// i = 0..3, columns 16 (l & 7) .. +15 of the block: each load instruction of a warp reads
+// four full 256-byte row segments.
+struct WBlockRegs {
+    uint32_t v[4][8];
+};
+__device__ __forceinline__ void wq_load(const uint16_t* __restrict__ w, int64_t n, int64_t k,
+                                        int64_t ld_w, int64_t nbk, int64_t blk, WBlockRegs& d) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bi = blk / nbk, bj = blk - (blk / nbk) * nbk;
+    const int64_t col = bj * 128 + (lane & 7) * 16;
+    const int64_t row0 = bi * 128 + warp * 16 + (lane >> 3);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t row = row0 + 4 * i;
+        if (col < k && row < n) {
+            ld_v8(w + row * ld_w + col, d.v[i]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) d.v[i][j] = 0u;
+        }
+    }
+}
+__device__ __forceinline__ void wq_process(const WBlockRegs& d, int64_t n, int64_t k, uint8_t* __restrict__ q,
+                                           int64_t ld_q, float* __restrict__ scales, int64_t ld_s,
+                                           int64_t nbk, int64_t blk, uint32_t* red,
+                                           int32_t* __restrict__ nonfinite_flag) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bi = blk / nbk, bj = blk - (blk / nbk) * nbk;
+    const int64_t col = bj * 128 + (lane & 7) * 16;
+    const int64_t row0 = bi * 128 + warp * 16 + (lane >> 3);
+    uint32_t ab = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ab = max(ab, abs_max_bits16(d.v[i]));
+    ab = __reduce_max_sync(0xFFFFFFFFu, ab);
+    if (lane == 0) red[warp] = ab;
+    __syncthreads();
+    ab = red[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) ab = max(ab, red[i]);
+    const float s = scale_from_amax_bits(ab);
+    if (threadIdx.x == 0) {
+        scales[bi * ld_s + bj] = s;
+        if (ab >= kNonFiniteBits && nonfinite_flag != nullptr) *nonfinite_flag = 1;
+    }
+    const bool col_ok = col < k;
+    if (ab >= kAmaxFastGuardBits) {
+        const float r = __frcp_rn(s);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t row = row0 + 4 * i;
+            if (col_ok && row < n) st_v4_na(q + row * ld_q + col, encode16<true>(d.v[i], s, r));
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t row = row0 + 4 * i;
+            if (col_ok && row < n) st_v4_na(q + row * ld_q + col, encode16<false>(d.v[i], s, 0.0f));
+        }
+    }
+}
+__global__ void __launch_bounds__(256, 2) weight_blockwise_wide_kernel(
+    const uint16_t* __restrict__ w, int64_t n, int64_t k, int64_t ld_w, uint8_t* __restrict__ q,
+    int64_t ld_q, float* __restrict__ scales, int64_t ld_s, int64_t nbk, int64_t nblocks,
+    int32_t* __restrict__ nonfinite_flag) {
+    __shared__ uint32_t red[2][8];
+    WBlockRegs a, b;
+    int64_t blk = blockIdx.x;
+    if (blk < nblocks) wq_load(w, n, k, ld_w, nbk, blk, a);
+    while (blk < nblocks) {  // unrolled by two so the register buffers stay static
+        int64_t nxt = blk + gridDim.x;
+        if (nxt < nblocks) wq_load(w, n, k, ld_w, nbk, nxt, b);
+        wq_process(a, n, k, q, ld_q, scales, ld_s, nbk, blk, red[0], nonfinite_flag);
+        blk = nxt;
+        if (blk >= nblocks) break;
+        nxt = blk + gridDim.x;
+        if (nxt < nblocks) wq_load(w, n, k, ld_w, nbk, nxt, a);
+        wq_process(b, n, k, q, ld_q, scales, ld_s, nbk, blk, red[1], nonfinite_flag);
+        blk = nxt;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Activations, wide path: requires x 32-byte aligned with ld_x % 16 == 0, codes 16-byte
+// aligned with ld_q % 16 == 0.  A warp item = (token row, 16 groups = 2048 channels); vector
+// j of lane l covers group 4j + (l >> 3) of the item, channels 16 (l & 7) .. +15 of it; eight
+// lanes reduce a group's amax with three xor-shuffles.  Warps are persistent over items and
+// prefetch their next item.
+struct AItemRegs {
+    uint32_t v[4][8];
+};
+__device__ __forceinline__ void aq_load(const uint16_t* __restrict__ x, int64_t ld_x, int64_t groups,
+                                        int64_t chunks, int64_t item, AItemRegs& d) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = item / chunks, chunk = item - (item / chunks) * chunks;
+    const uint16_t* xr = x + row * ld_x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t g = chunk * 16 + 4 * j + (lane >> 3);
+        if (g < groups) {
+            ld_v8(xr + g * 128 + (lane & 7) * 16, d.v[j]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) d.v[j][t] = 0u;
+        }
+    }
+}
+__device__ __forceinline__ void aq_process(const AItemRegs& d, uint8_t* __restrict__ q, int64_t ld_q,
+                                           float* __restrict__ scales, int64_t ld_s, int64_t groups,
+                                           int64_t chunks, int64_t item, int32_t* __restrict__ nonfinite_flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = item / chunks, chunk = item - (item / chunks) * chunks;
+    uint32_t ab[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ab[j] = abs_max_bits16(d.v[j]);
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ab[j] = max(ab[j], __shfl_xor_sync(0xFFFFFFFFu, ab[j], off));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t g = chunk * 16 + 4 * j + (lane >> 3);
+        if (g >= groups) continue;
+        const float s = scale_from_amax_bits(ab[j]);
+        if ((lane & 7) == 0) {
+            scales[g * ld_s + row] = s;
+            if (ab[j] >= kNonFiniteBits && nonfinite_flag != nullptr) *nonfinite_flag = 1;
+        }
+        uint4 c;
+        if (ab[j] >= kAmaxFastGuardBits)
+            c = encode16<true>(d.v[j], s, __frcp_rn(s));
+        else
+            c = encode16<false>(d.v[j], s, 0.0f);
+        st_v4_na(q + row * ld_q + g * 128 + (lane & 7) * 16, c);
+    }
+}
+__global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
+    const uint16_t* __restrict__ x, int64_t ld_x, uint8_t* __restrict__ q, int64_t ld_q,
+    float* __restrict__ scales, int64_t ld_s, int64_t groups, int64_t chunks, int64_t items,
+    int32_t* __restrict__ nonfinite_flag) {
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
+    int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    AItemRegs a, b;
+    if (item < items) aq_load(x, ld_x, groups, chunks, item, a);
+    while (item < items) {
+        int64_t nxt = item + warps;
+        if (nxt < items) aq_load(x, ld_x, groups, chunks, nxt, b);
+        aq_process(a, q, ld_q, scales, ld_s, groups, chunks, item, nonfinite_flag);
+        item = nxt;
+        if (item >= items) break;
+        nxt = item + warps;
+        if (nxt < items) aq_load(x, ld_x, groups, chunks, nxt, a);
+        aq_process(b, q, ld_q, scales, ld_s, groups, chunks, item, nonfinite_flag);
+        item = nxt;
+    }
+}
+
+int sm_count() {
+    static int sms = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return sms;
+}
+
+inline bool al(const void* p, uintptr_t a) { return reinterpret_cast<uintptr_t>(p) % a == 0; }
+
 }  // namespace
 
 cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int64_t ld_w,
@@ -187,8 +428,14 @@ cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int
     const int64_t blocks = nbn * nbk;
     if (blocks == 0) return cudaSuccess;
     if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
-    weight_blockwise_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-        w, n, k, ld_w, q, ld_q, scales, ld_s, nbk, flag);
+    if (k % 16 == 0 && al(w, 32) && ld_w % 16 == 0 && al(q, 16) && ld_q % 16 == 0) {
+        const int64_t grid = blocks < 2LL * sm_count() ? blocks : 2LL * sm_count();
+        weight_blockwise_wide_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(
+            w, n, k, ld_w, q, ld_q, scales, ld_s, nbk, blocks, flag);
+    } else {
+        weight_blockwise_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+            w, n, k, ld_w, q, ld_q, scales, ld_s, nbk, flag);
+    }
     return cudaGetLastError();
 }
 
@@ -201,8 +448,17 @@ cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, 
     if (items == 0) return cudaSuccess;
     const int64_t blocks = (items + 7) / 8;
     if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
-    act_per_token_group_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-        x, m, k, ld_x, q, ld_q, scales, ld_s, chunks, flag);
+    if (al(x, 32) && ld_x % 16 == 0 && al(q, 16) && ld_q % 16 == 0) {
+        const int64_t wchunks = (groups + 15) / 16;
+        const int64_t witems = m * wchunks;
+        const int64_t wblocks = (witems + 7) / 8;
+        const int64_t grid = wblocks < 2LL * sm_count() ? wblocks : 2LL * sm_count();
+        act_per_token_group_wide_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(
+            x, ld_x, q, ld_q, scales, ld_s, groups, wchunks, witems, flag);
+    } else {
+        act_per_token_group_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+            x, m, k, ld_x, q, ld_q, scales, ld_s, chunks, flag);
+    }
     return cudaGetLastError();
 }
 

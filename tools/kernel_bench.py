@@ -24,12 +24,22 @@ HBM = PEAKS["hbm_gbs"]
 FP8 = 2 * PEAKS["bf16_tflops"]
 
 
+FLUSH_MODE = "write"
+
+
+def do_flush(flush):
+    if FLUSH_MODE == "write":
+        flush.zero_()  # dirty lines: the next kernel also pays their write-back
+    elif FLUSH_MODE == "read":
+        flush.view(torch.int64).sum()  # clean eviction: L2 left holding read-only lines
+
+
 def timeit(fn, iters, flush):
     ts = []
     for _ in range(3):
         fn()
     for _ in range(iters):
-        flush.zero_()
+        do_flush(flush)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
@@ -45,7 +55,10 @@ def main():
     ap.add_argument("--what", default="all")
     ap.add_argument("--decode", action="store_true")
     ap.add_argument("--moe", action="store_true")
+    ap.add_argument("--flush", choices=["write", "read", "none"], default="write")
     args = ap.parse_args()
+    global FLUSH_MODE
+    FLUSH_MODE = args.flush
     dev = torch.device("cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     g = torch.Generator(device=dev)
