@@ -81,6 +81,29 @@ fp8q_status quantize_weight_blockwise(const void* w_bf16, int64_t n, int64_t k, 
                                       int32_t* nonfinite_flag, void* stream);
 
 /*
+ * quantize_weight_blockwise_batched -- the per-step weight synchronisation of PAPER.md:72
+ * re-quantizes every in-scope linear weight; this entry point does exactly what `count`
+ * quantize_weight_blockwise calls would do, but in as few kernel launches as possible (up to
+ * 16 tensors per launch), so small tensors do not each pay a launch and a pipeline ramp.
+ *   tensors  HOST array of `count` descriptors (read during the call only); the pointers in
+ *            them are device pointers with the meaning and requirements of
+ *            quantize_weight_blockwise.  Every descriptor is validated before anything is
+ *            enqueued; the first failing one determines the status.
+ *   nonfinite_flag, stream  as quantize_weight_blockwise (one flag for the whole batch).
+ */
+typedef struct {
+    const void* w_bf16;
+    int64_t n, k, ld_w;
+    uint8_t* codes;
+    int64_t ld_q;
+    float* scales;
+    int64_t ld_s;
+} fp8q_weight_tensor;
+
+fp8q_status quantize_weight_blockwise_batched(const fp8q_weight_tensor* tensors, int32_t count,
+                                              int32_t* nonfinite_flag, void* stream);
+
+/*
  * quantize_act_per_token_group -- dynamic activation quantization, PAPER.md:46,65,73;
  * granularity 1x128 (per token m, per 128-channel group g).
  *   x_bf16  [m, k] BF16, row stride ld_x.

@@ -13,5 +13,6 @@ from .fp8q import (  # noqa: F401
     load_library,
     quantize_act_per_token_group,
     quantize_weight_blockwise,
+    quantize_weight_blockwise_batched,
     version,
 )

@@ -55,24 +55,59 @@ int64_t fp8q_kernel_launches(void) { return g_launches.load(); }
 
 void fp8q_debug_set_gemm_trace(uint32_t* dev_ptr) { fp8q::set_gemm_trace(dev_ptr); }
 
-fp8q_status quantize_weight_blockwise(const void* w_bf16, int64_t n, int64_t k, int64_t ld_w,
-                                      uint8_t* codes, int64_t ld_q, float* scales, int64_t ld_s,
-                                      int32_t* nonfinite_flag, void* stream) {
+static fp8q_status check_weight(const void* w_bf16, int64_t n, int64_t k, int64_t ld_w, const uint8_t* codes,
+                                int64_t ld_q, const float* scales, int64_t ld_s) {
     if (n < 0 || k < 0) return FP8Q_EINVAL;
     if (ld_w < k || ld_q < k || ld_s < (k + 127) / 128) return FP8Q_EINVAL;
     if (n == 0 || k == 0) return FP8Q_OK;
     if (w_bf16 == nullptr || codes == nullptr || scales == nullptr) return FP8Q_EINVAL;
     if (k % 8 != 0) return FP8Q_ESHAPE;
-    if (!aligned(w_bf16, 16) || ld_w % 8 != 0 || !aligned(codes, 8) || ld_q % 8 != 0 ||
-        !aligned(scales, 4) || (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)))
+    if (!aligned(w_bf16, 16) || ld_w % 8 != 0 || !aligned(codes, 8) || ld_q % 8 != 0 || !aligned(scales, 4))
         return FP8Q_EALIGN;
-    fp8q_status st = check_device();
+    return FP8Q_OK;
+}
+
+fp8q_status quantize_weight_blockwise(const void* w_bf16, int64_t n, int64_t k, int64_t ld_w,
+                                      uint8_t* codes, int64_t ld_q, float* scales, int64_t ld_s,
+                                      int32_t* nonfinite_flag, void* stream) {
+    fp8q_status st = check_weight(w_bf16, n, k, ld_w, codes, ld_q, scales, ld_s);
+    if (st != FP8Q_OK || n == 0 || k == 0) return st;
+    if (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)) return FP8Q_EALIGN;
+    st = check_device();
     if (st != FP8Q_OK) return st;
     cudaError_t e = fp8q::launch_weight_blockwise(static_cast<const uint16_t*>(w_bf16), n, k, ld_w,
                                                   codes, ld_q, scales, ld_s, nonfinite_flag,
                                                   static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) g_launches.fetch_add(1);
     return from_cuda(e);
+}
+
+fp8q_status quantize_weight_blockwise_batched(const fp8q_weight_tensor* tensors, int32_t count,
+                                              int32_t* nonfinite_flag, void* stream) {
+    if (count < 0 || (count > 0 && tensors == nullptr)) return FP8Q_EINVAL;
+    if (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)) return FP8Q_EALIGN;
+    for (int32_t i = 0; i < count; ++i) {
+        const fp8q_weight_tensor& t = tensors[i];
+        fp8q_status st = check_weight(t.w_bf16, t.n, t.k, t.ld_w, t.codes, t.ld_q, t.scales, t.ld_s);
+        if (st != FP8Q_OK) return st;
+    }
+    if (count == 0) return FP8Q_OK;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    // chunks of kMaxWeightBatch descriptors on the stack (no host allocation, nothing can throw)
+    fp8q::WeightDesc d[fp8q::kMaxWeightBatch];
+    for (int32_t base = 0; base < count; base += fp8q::kMaxWeightBatch) {
+        const int32_t c = count - base < fp8q::kMaxWeightBatch ? count - base : fp8q::kMaxWeightBatch;
+        for (int32_t i = 0; i < c; ++i) {
+            const fp8q_weight_tensor& t = tensors[base + i];
+            d[i] = fp8q::WeightDesc{static_cast<const uint16_t*>(t.w_bf16), t.n, t.k, t.ld_w, t.codes, t.ld_q,
+                                    t.scales, t.ld_s};
+        }
+        cudaError_t e = fp8q::launch_weight_blockwise_batch(d, c, nonfinite_flag, static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return FP8Q_ECUDA;
+        g_launches.fetch_add(fp8q::weight_batch_launches(d, c));
+    }
+    return FP8Q_OK;
 }
 
 fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t k, int64_t ld_x,

@@ -256,6 +256,18 @@ __device__ __forceinline__ uint4 encode16(const uint32_t (&w)[8], float s, float
 struct WBlockRegs {
     uint32_t v[4][8];
 };
+struct WTensor {
+    const uint16_t* w;
+    uint8_t* q;
+    float* scales;
+    int64_t n, k, ld_w, ld_q, ld_s, nbk;
+    int64_t blk0;  // first global block index of this tensor
+};
+struct WBatch {
+    WTensor t[kMaxWeightBatch];
+    int count;
+    int64_t nblocks;
+};
 __device__ __forceinline__ void wq_load(const uint16_t* __restrict__ w, int64_t n, int64_t k,
                                         int64_t ld_w, int64_t nbk, int64_t blk, WBlockRegs& d) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -311,23 +323,37 @@ __device__ __forceinline__ void wq_process(const WBlockRegs& d, int64_t n, int64
         }
     }
 }
-__global__ void __launch_bounds__(256, 2) weight_blockwise_wide_kernel(
-    const uint16_t* __restrict__ w, int64_t n, int64_t k, int64_t ld_w, uint8_t* __restrict__ q,
-    int64_t ld_q, float* __restrict__ scales, int64_t ld_s, int64_t nbk, int64_t nblocks,
-    int32_t* __restrict__ nonfinite_flag) {
+// A batch of weight tensors quantized by ONE launch (the weight sync re-quantizes every
+// linear weight of a layer at once: one launch instead of one per tensor).
+__global__ void __launch_bounds__(256, 2) weight_blockwise_wide_kernel(const __grid_constant__ WBatch bt,
+                                                                        int32_t* __restrict__ nonfinite_flag) {
     __shared__ uint32_t red[2][8];
     WBlockRegs a, b;
+    const int64_t nblocks = bt.nblocks;
+    auto tensor_of = [&](int64_t blk) {
+        int i = 0;
+        while (i + 1 < bt.count && blk >= bt.t[i + 1].blk0) ++i;
+        return i;
+    };
+    auto load = [&](int64_t blk, WBlockRegs& d) {
+        const WTensor& t = bt.t[tensor_of(blk)];
+        wq_load(t.w, t.n, t.k, t.ld_w, t.nbk, blk - t.blk0, d);
+    };
+    auto process = [&](int64_t blk, const WBlockRegs& d, uint32_t* rd) {
+        const WTensor& t = bt.t[tensor_of(blk)];
+        wq_process(d, t.n, t.k, t.q, t.ld_q, t.scales, t.ld_s, t.nbk, blk - t.blk0, rd, nonfinite_flag);
+    };
     int64_t blk = blockIdx.x;
-    if (blk < nblocks) wq_load(w, n, k, ld_w, nbk, blk, a);
+    if (blk < nblocks) load(blk, a);
     while (blk < nblocks) {  // unrolled by two so the register buffers stay static
         int64_t nxt = blk + gridDim.x;
-        if (nxt < nblocks) wq_load(w, n, k, ld_w, nbk, nxt, b);
-        wq_process(a, n, k, q, ld_q, scales, ld_s, nbk, blk, red[0], nonfinite_flag);
+        if (nxt < nblocks) load(nxt, b);
+        process(blk, a, red[0]);
         blk = nxt;
         if (blk >= nblocks) break;
         nxt = blk + gridDim.x;
-        if (nxt < nblocks) wq_load(w, n, k, ld_w, nbk, nxt, a);
-        wq_process(b, n, k, q, ld_q, scales, ld_s, nbk, blk, red[1], nonfinite_flag);
+        if (nxt < nblocks) load(nxt, a);
+        process(blk, b, red[1]);
         blk = nxt;
     }
 }
@@ -419,24 +445,75 @@ int sm_count() {
 
 inline bool al(const void* p, uintptr_t a) { return reinterpret_cast<uintptr_t>(p) % a == 0; }
 
+bool wide_ok(const WeightDesc& d) {
+    return d.k % 16 == 0 && al(d.w, 32) && d.ld_w % 16 == 0 && al(d.q, 16) && d.ld_q % 16 == 0;
+}
+
 }  // namespace
+
+cudaError_t launch_weight_blockwise_batch(const WeightDesc* descs, int count, int32_t* flag,
+                                          cudaStream_t stream) {
+    // wide path for every aligned tensor, batched kMaxWeightBatch per launch
+    WBatch bt{};
+    bt.count = 0;
+    bt.nblocks = 0;
+    auto flush = [&]() -> cudaError_t {
+        if (bt.count == 0) return cudaSuccess;
+        const int64_t cap = 2LL * sm_count();
+        const int64_t grid = bt.nblocks < cap ? bt.nblocks : cap;
+        if (grid > 0) weight_blockwise_wide_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(bt, flag);
+        bt.count = 0;
+        bt.nblocks = 0;
+        return cudaGetLastError();
+    };
+    for (int i = 0; i < count; ++i) {
+        const WeightDesc& d = descs[i];
+        const int64_t nbn = (d.n + 127) / 128, nbk = (d.k + 127) / 128;
+        const int64_t blocks = nbn * nbk;
+        if (blocks == 0) continue;
+        if (wide_ok(d)) {
+            WTensor& t = bt.t[bt.count++];
+            t.w = d.w;
+            t.q = d.q;
+            t.scales = d.scales;
+            t.n = d.n;
+            t.k = d.k;
+            t.ld_w = d.ld_w;
+            t.ld_q = d.ld_q;
+            t.ld_s = d.ld_s;
+            t.nbk = nbk;
+            t.blk0 = bt.nblocks;
+            bt.nblocks += blocks;
+            if (bt.count == kMaxWeightBatch) {
+                cudaError_t e = flush();
+                if (e != cudaSuccess) return e;
+            }
+        } else {
+            if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
+            weight_blockwise_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+                d.w, d.n, d.k, d.ld_w, d.q, d.ld_q, d.scales, d.ld_s, nbk, flag);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return flush();
+}
+
+int weight_batch_launches(const WeightDesc* descs, int count) {
+    int wide = 0, narrow = 0;
+    for (int i = 0; i < count; ++i) {
+        const WeightDesc& d = descs[i];
+        if (d.n == 0 || d.k == 0) continue;
+        if (wide_ok(d)) ++wide; else ++narrow;
+    }
+    return narrow + (wide + kMaxWeightBatch - 1) / kMaxWeightBatch;
+}
 
 cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int64_t ld_w,
                                     uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
                                     int32_t* flag, cudaStream_t stream) {
-    const int64_t nbn = (n + 127) / 128, nbk = (k + 127) / 128;
-    const int64_t blocks = nbn * nbk;
-    if (blocks == 0) return cudaSuccess;
-    if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
-    if (k % 16 == 0 && al(w, 32) && ld_w % 16 == 0 && al(q, 16) && ld_q % 16 == 0) {
-        const int64_t grid = blocks < 2LL * sm_count() ? blocks : 2LL * sm_count();
-        weight_blockwise_wide_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(
-            w, n, k, ld_w, q, ld_q, scales, ld_s, nbk, blocks, flag);
-    } else {
-        weight_blockwise_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-            w, n, k, ld_w, q, ld_q, scales, ld_s, nbk, flag);
-    }
-    return cudaGetLastError();
+    const WeightDesc d{w, n, k, ld_w, q, ld_q, scales, ld_s};
+    return launch_weight_blockwise_batch(&d, 1, flag, stream);
 }
 
 cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, int64_t ld_x,

@@ -5,6 +5,23 @@
 
 namespace fp8q {
 
+constexpr int kMaxWeightBatch = 16;  // tensors per batched weight-quantization launch
+
+struct WeightDesc {
+    const uint16_t* w;
+    int64_t n, k, ld_w;
+    uint8_t* q;
+    int64_t ld_q;
+    float* scales;
+    int64_t ld_s;
+};
+
+// All descs in as few launches as possible (kMaxWeightBatch wide-path tensors per launch;
+// tensors that miss the wide path's alignment get their own launch of the general kernel).
+cudaError_t launch_weight_blockwise_batch(const WeightDesc* descs, int count, int32_t* flag,
+                                          cudaStream_t stream);
+int weight_batch_launches(const WeightDesc* descs, int count);
+
 cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int64_t ld_w,
                                     uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
                                     int32_t* flag, cudaStream_t stream);

@@ -25,6 +25,13 @@ _lock = threading.Lock()
 _lib = None
 
 
+class WeightTensorDesc(ctypes.Structure):
+    """fp8q_weight_tensor (include/fp8q.h)."""
+    _fields_ = [("w_bf16", ctypes.c_void_p), ("n", ctypes.c_int64), ("k", ctypes.c_int64),
+                ("ld_w", ctypes.c_int64), ("codes", ctypes.c_void_p), ("ld_q", ctypes.c_int64),
+                ("scales", ctypes.c_void_p), ("ld_s", ctypes.c_int64)]
+
+
 class Fp8qError(RuntimeError):
     """A libfp8q entry point returned a non-OK fp8q_status."""
 
@@ -47,6 +54,8 @@ def load_library() -> ctypes.CDLL:
         lib.fp8q_kernel_launches.restype = I64
         lib.quantize_weight_blockwise.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
         lib.quantize_weight_blockwise.restype = ctypes.c_int
+        lib.quantize_weight_blockwise_batched.argtypes = [ctypes.POINTER(WeightTensorDesc), I32, P, P]
+        lib.quantize_weight_blockwise_batched.restype = ctypes.c_int
         lib.quantize_act_per_token_group.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
         lib.quantize_act_per_token_group.restype = ctypes.c_int
         lib.fp8_block_gemm_workspace_size.argtypes = [I64, I64, I64]
@@ -120,6 +129,26 @@ def quantize_weight_blockwise(w: torch.Tensor, codes: torch.Tensor | None = None
         w.data_ptr(), n, k, _ld(w), codes.data_ptr(), _ld(codes), scales.data_ptr(), _ld(scales),
         flag, _stream(stream)), "quantize_weight_blockwise")
     return codes, scales
+
+
+def quantize_weight_blockwise_batched(items, nonfinite_flag: torch.Tensor | None = None, stream=None):
+    """Several blockwise weight quantizations (Eq. (1)) in as few launches as possible -- the
+    per-step weight sync of PAPER.md:72.  items: sequence of (w, codes, scales) CUDA tensors
+    with the shapes of quantize_weight_blockwise's inputs/outputs."""
+    items = list(items)
+    arr = (WeightTensorDesc * max(1, len(items)))()
+    for i, (w, codes, scales) in enumerate(items):
+        _cuda2d(w, "w", torch.bfloat16)
+        _cuda2d(codes, "codes", torch.uint8)
+        _cuda2d(scales, "scales", torch.float32)
+        n, k = w.shape
+        if codes.shape != (n, k) or scales.shape[0] < (n + 127) // 128 or scales.shape[1] < (k + 127) // 128:
+            raise Fp8qError(f"item {i}: output shape mismatch")
+        arr[i] = WeightTensorDesc(w.data_ptr(), n, k, _ld(w), codes.data_ptr(), _ld(codes),
+                                  scales.data_ptr(), _ld(scales))
+    flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
+    _check(load_library().quantize_weight_blockwise_batched(arr, len(items), flag, _stream(stream)),
+           "quantize_weight_blockwise_batched")
 
 
 def act_scales_ld(m: int) -> int:

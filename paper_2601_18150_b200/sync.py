@@ -151,7 +151,20 @@ class WeightSyncEngine:
         missing = [s.name for s in self.specs if s.name not in shards]
         if missing:
             raise KeyError(f"missing shards: {missing}")
-        if comm_stream is None or self.world == 1:
+        if self.quantize_fn is _default_quantize and (comm_stream is None or self.world == 1):
+            # one batched launch for every local shard (the whole layer's weights)
+            from .fp8q import quantize_weight_blockwise_batched
+            items = []
+            for s in self.specs:
+                sh = self.my_shard(s.name)
+                w = shards[s.name]
+                if w.shape[0] != sh.row1 - sh.row0:
+                    raise ValueError(f"{s.name}: shard has {w.shape[0]} rows, plan says {sh.row1 - sh.row0}")
+                items.append((w, self.codes[s.name][sh.row0:sh.row1], self.scales[s.name][sh.srow0:sh.srow1]))
+            quantize_weight_blockwise_batched(items)
+            for s in self.specs:
+                self.gather(s.name)
+        elif comm_stream is None or self.world == 1:
             for s in self.specs:
                 self.quantize_local(s.name, shards[s.name])
                 self.gather(s.name)

@@ -160,3 +160,29 @@ def test_quantizers_deterministic():
     c1, s1 = fp8q.quantize_weight_blockwise(w)
     c2, s2 = fp8q.quantize_weight_blockwise(w)
     assert torch.equal(c1, c2) and torch.equal(s1, s2)
+
+
+def test_weight_batched_equals_individual():
+    # quantize_weight_blockwise_batched (one launch per <=16 tensors): bitwise what the
+    # per-tensor calls produce, incl. a misaligned tensor (general kernel) and > 16 tensors.
+    shapes = [(6144 // 8, 512), (256, 384), (300, 208), (128, 1024)] * 5
+    items, refs = [], []
+    for i, (n, k) in enumerate(shapes):
+        bits = synth.qwen3_weight(n, k, seed=100 + i)
+        if i == 2:
+            big = np.zeros((n, k + 8), np.uint16)
+            big[:, :k] = bits
+            w = to_dev_bf16(big)[:, :k]          # ld_w = k + 8: not 32-byte aligned rows
+        else:
+            w = to_dev_bf16(bits)
+        codes = torch.empty((n, k), dtype=torch.uint8, device="cuda")
+        scales = torch.empty(((n + 127) // 128, (k + 127) // 128), dtype=torch.float32, device="cuda")
+        items.append((w, codes, scales))
+        refs.append(oracle.quantize_weight_blockwise(bits))
+    before = fp8q.kernel_launches()
+    fp8q.quantize_weight_blockwise_batched(items)
+    torch.cuda.synchronize()
+    assert fp8q.kernel_launches() - before == 3  # 19 wide tensors -> 2 launches, 1 general
+    for (w, codes, scales), (oc, os_) in zip(items, refs):
+        assert np.array_equal(to_host_u8(codes), oc)
+        assert np.array_equal(to_host_f32(scales), os_)
