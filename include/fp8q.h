@@ -129,14 +129,19 @@ fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t 
  *   b        [n, k] E4M3 codes (K-major, nn.Linear weight), row stride ld_b bytes.
  *   b_scales [ceil(n/128)][ld_sb] fp32 (as written by quantize_weight_blockwise), ld_sb >= k/128.
  *   d        [m, n] out, BF16 or F32 per d_dtype, row stride ld_d elements.
- *   workspace / workspace_bytes: see fp8_block_gemm_workspace_size (currently 0 bytes;
- *           workspace may be NULL when 0 is required).
+ *   workspace / workspace_bytes: optional (NULL / 0 allowed).  With at least
+ *           fp8_block_gemm_workspace_size(m, n, k) bytes (256-byte aligned, ZERO-FILLED before
+ *           its first use; every launch leaves it zeroed again), small-M problems (decode,
+ *           M < 256) split the K loop over more CTAs: slices park fp32 partials in the
+ *           workspace and the last slice of each tile sums them in slice order
+ *           (deterministic).  Without it the same problem runs unsplit (slower, equally
+ *           correct).  A workspace must not be shared by concurrently running GEMMs.
  *   Requirements: k % 128 == 0, n % 8 == 0 (ESHAPE); a, b 16-byte aligned with ld_a % 16 ==
  *     0 and ld_b % 16 == 0 (TMA); d 16-byte aligned with ld_d * sizeof(out) % 16 == 0;
  *     a_scales/b_scales 4-byte aligned (EALIGN).  m == 0 or n == 0 is a no-op; k == 0 writes 0.
  *   Work: 2*m*n*k FLOP on the tensor cores (kind::f8f6f4), m*n*k/128 fp32 promotion FMAs.
  */
-size_t fp8_block_gemm_workspace_size(int64_t m, int64_t n, int64_t k);
+size_t fp8_block_gemm_workspace_size(int64_t m, int64_t n, int64_t k); /* 0: never splits */
 fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales, int64_t ld_sa,
                            const uint8_t* b, int64_t ld_b, const float* b_scales, int64_t ld_sb,
                            void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,

@@ -131,7 +131,9 @@ fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t 
     return from_cuda(e);
 }
 
-size_t fp8_block_gemm_workspace_size(int64_t, int64_t, int64_t) { return 0; }
+size_t fp8_block_gemm_workspace_size(int64_t m, int64_t n, int64_t k) {
+    return fp8q::gemm_workspace_bytes(m, n, k, false);
+}
 
 size_t fp8_block_gemm_grouped_workspace_size(int64_t, int64_t, int64_t, int32_t) { return 0; }
 
@@ -165,8 +167,7 @@ fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales
                            const uint8_t* b, int64_t ld_b, const float* b_scales, int64_t ld_sb,
                            void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
                            int64_t k, void* workspace, size_t workspace_bytes, void* stream) {
-    (void)workspace;
-    (void)workspace_bytes;
+    if (workspace != nullptr && !aligned(workspace, 256)) return FP8Q_EALIGN;
     fp8q_status st = gemm_common_checks(a, ld_a, a_scales, ld_sa, b, ld_b, b_scales, ld_sb, d, ld_d,
                                         d_dtype, m, n, k);
     if (st != FP8Q_OK || m == 0 || n == 0) return st;
@@ -190,6 +191,8 @@ fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales
     g.k = k;
     g.offsets = nullptr;
     g.groups = 1;
+    g.workspace = workspace;
+    g.workspace_bytes = workspace_bytes;
     int launched = 0;
     cudaError_t e = fp8q::launch_fp8_block_gemm(g, static_cast<cudaStream_t>(stream), &launched);
     g_launches.fetch_add(launched);
@@ -234,6 +237,8 @@ fp8q_status fp8_block_gemm_grouped(const uint8_t* a, int64_t ld_a, const float* 
     g.k = k;
     g.offsets = offsets_dev;
     g.groups = num_groups;
+    g.workspace = nullptr;
+    g.workspace_bytes = 0;
     int launched = 0;
     cudaError_t e = fp8q::launch_fp8_block_gemm(g, static_cast<cudaStream_t>(stream), &launched);
     g_launches.fetch_add(launched);

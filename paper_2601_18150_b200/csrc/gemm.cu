@@ -89,6 +89,9 @@ struct KParams {
     int num_kb;
     int num_n_tiles;
     const int32_t* offsets;  // nullptr: one group of m rows
+    int splits;              // split-K slices per tile (one-CTA kernel, dense, small M); 1 = off
+    float* ws;               // split-K partials [tile][split][128][BN] fp32
+    int32_t* counters;       // split-K arrival counters [tile], zero between launches
     uint32_t* trace;         // dev-only timeline (fp8q_debug_set_trace), nullptr in production
     int debug_mode;          // dev-only: 1 = promotion skips TMEM loads + FMAs (MMA pipe ceiling),
                              // 2 = also no TMA after the first stages (tensor-core-only ceiling)
@@ -167,6 +170,9 @@ struct EpiTile {
     int64_t row_end;  // end of the rows this tile may write (group end / m)
     int64_t col0;     // first of this thread's columns
     int g;            // group (MoE expert) index
+    int kb0, kb1;     // this work item's k-block range
+    int64_t tile;     // linear tile index (split-K bookkeeping)
+    int split;        // split-K slice of this work item
 };
 // The first two k-blocks' (sa, sb) of a tile: loaded one tile ahead so the HBM/L2 latency of
 // the first scales overlaps the previous tile's last k-blocks and stores.
@@ -176,19 +182,42 @@ struct ScalePre {
 __device__ __forceinline__ bool tile_live(const KParams& p, const EpiTile& t) {
     return t.row < t.row_end && t.col0 < p.n;
 }
-__device__ __forceinline__ ScalePre prefetch_scales(const KParams& p, const EpiTile& t) {
+// Where a tile's first two k-blocks' scales live (computed once, so only two pointers and a
+// flag -- not the whole next tile -- stay live across the k-loop).
+struct ScalePtrs {
+    const float* sap;
+    const float* sbp;
+    int64_t ld_sa;
+    bool live;
+    bool two;
+};
+__device__ __forceinline__ ScalePtrs scale_ptrs(const KParams& p, const EpiTile& t) {
+    ScalePtrs q;
+    q.live = tile_live(p, t);
+    q.two = t.kb1 - t.kb0 > 1;
+    q.ld_sa = p.ld_sa;
+    q.sap = p.sa + t.row + int64_t(t.kb0) * p.ld_sa;
+    q.sbp = p.sb + int64_t(t.g) * p.stride_sb + (t.col0 / 128) * p.ld_sb + t.kb0;
+    return q;
+}
+__device__ __forceinline__ ScalePre load_scales(const ScalePtrs& q) {
     ScalePre s{0.f, 0.f, 0.f, 0.f};
-    if (tile_live(p, t)) {
-        const float* sap = p.sa + t.row;
-        const float* sbp = p.sb + int64_t(t.g) * p.stride_sb + (t.col0 / 128) * p.ld_sb;
-        s.sa0 = __ldg(sap);
-        s.sb0 = __ldg(sbp);
-        if (p.num_kb > 1) {
-            s.sa1 = __ldg(sap + p.ld_sa);
-            s.sb1 = __ldg(sbp + 1);
+    if (q.live) {
+        s.sa0 = __ldg(q.sap);
+        s.sb0 = __ldg(q.sbp);
+        if (q.two) {
+            s.sa1 = __ldg(q.sap + q.ld_sa);
+            s.sb1 = __ldg(q.sbp + 1);
         }
     }
     return s;
+}
+__device__ __forceinline__ ScalePre prefetch_scales(const KParams& p, const EpiTile& t) {
+    return load_scales(scale_ptrs(p, t));
+}
+
+__device__ __forceinline__ int split_begin(const KParams& p, int s) {
+    return static_cast<int>((static_cast<int64_t>(s) * p.num_kb) / p.splits);
 }
 
 // For every k-block: wait for the partial in TMEM buffer it % NBUF, tcgen05.ld it, hand the
@@ -215,15 +244,18 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
     // Scale prefetch two k-blocks ahead; the raw values are only multiplied when used,
     // so the load latency never sits between the TMEM-full wait and the FMAs.
     float sa0 = pre.sa0, sb0 = pre.sb0, sa1 = pre.sa1, sb1 = pre.sb1;
-    for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+    ScalePtrs nq = scale_ptrs(p, next);
+    nq.live = nq.live && has_next;
+    const int kb0 = tile.kb0, kb1 = tile.kb1;
+    for (int kb = kb0; kb < kb1; ++kb, ++it) {
         const float f = sa0 * sb0;
         sa0 = sa1;
         sb0 = sb1;
-        if (live && kb + 2 < p.num_kb) {
+        if (live && kb + 2 < kb1) {
             sa1 = __ldg(sap + int64_t(kb + 2) * p.ld_sa);
             sb1 = __ldg(sbp + kb + 2);
         }
-        if (has_next && kb == (p.num_kb > 4 ? p.num_kb - 4 : 0)) next_pre = prefetch_scales(p, next);
+        if (kb == (kb1 - kb0 > 4 ? kb1 - 4 : kb0)) next_pre = load_scales(nq);
         const uint32_t buf = it % NBUF;
         const uint32_t bph = (it / NBUF) & 1u;
         mbar_wait(&tfull[buf], bph);
@@ -258,7 +290,6 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    if (tr) trace_ev(p, it, 4);
                     if (PAIR)
                         mbar_arrive_cluster(&tempty[buf], 0);
                     else
@@ -270,6 +301,43 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
     }
     const bool tr_store = (threadIdx.x == EPI_WARP0 * 32);
     if (tr_store) trace_ev(p, it - 1, 6);
+    if (!PAIR && p.splits > 1) {
+        // ---- split-K: park this slice's fp32 partial; the last slice to arrive sums all
+        // slices in slice order (deterministic) and stores the tile.
+        __shared__ int sk_last;
+        const int r_in = qd * 32 + lane;  // row within the tile
+        float* mine = p.ws + ((tile.tile * p.splits + tile.split) * BM + r_in) * BN + h * EPI_COLS;
+        if (live) {  // only real rows/columns are parked and summed (decode: M << 128)
+#pragma unroll
+            for (int j = 0; j < EPI_COLS / 4; ++j)
+                st_v4(mine + 4 * j, __float_as_uint(acc[2 * j].x), __float_as_uint(acc[2 * j].y),
+                      __float_as_uint(acc[2 * j + 1].x), __float_as_uint(acc[2 * j + 1].y));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
+        if (threadIdx.x == EPI_WARP0 * 32) {
+            const int old = atomicAdd(&p.counters[tile.tile], 1);
+            __threadfence();
+            sk_last = (old == p.splits - 1);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
+        if (!sk_last) return;
+        const float* base = p.ws + (tile.tile * p.splits * BM + r_in) * BN + h * EPI_COLS;
+#pragma unroll
+        for (int j = 0; j < EPI_COLS / 2; ++j) acc[j] = make_float2(0.f, 0.f);
+        for (int sl = 0; sl < p.splits && live; ++sl) {
+            const float4* src = reinterpret_cast<const float4*>(base + int64_t(sl) * BM * BN);
+#pragma unroll
+            for (int j = 0; j < EPI_COLS / 4; ++j) {
+                const float4 v = __ldcg(src + j);
+                acc[2 * j].x += v.x;
+                acc[2 * j].y += v.y;
+                acc[2 * j + 1].x += v.z;
+                acc[2 * j + 1].y += v.w;
+            }
+        }
+        if (threadIdx.x == EPI_WARP0 * 32) p.counters[tile.tile] = 0;  // reusable workspace
+    }
     if (col0 >= p.n) return;  // warp-uniform: these columns are past the matrix
     // ---- output: the warp's 32 rows x EPI_COLS columns.  Full 32-row slices go through
     // swizzled smem chunks (32 rows x 64 B) and asynchronous TMA stores (the tensor map clips
@@ -409,10 +477,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
-            for (int64_t t = blockIdx.x; cur.seek(p, t, mt, nt); t += gridDim.x) {
+            for (int64_t item = blockIdx.x;; item += gridDim.x) {
+                if (!cur.seek(p, item / p.splits, mt, nt)) break;
+                const int sp = static_cast<int>(item % p.splits);
                 const int32_t arow = static_cast<int32_t>(cur.row0 + int64_t(mt) * BM);
                 const int32_t brow = nt * BN;
-                for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+                for (int kb = split_begin(p, sp); kb < split_begin(p, sp + 1); ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
                     if (p.debug_mode == 2 && it >= STAGES) break;  // dev: operands stay resident
@@ -432,8 +502,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
-            for (int64_t t = blockIdx.x; cur.seek(p, t, mt, nt); t += gridDim.x) {
-                for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+            for (int64_t item = blockIdx.x;; item += gridDim.x) {
+                if (!cur.seek(p, item / p.splits, mt, nt)) break;
+                const int sp = static_cast<int>(item % p.splits);
+                for (int kb = split_begin(p, sp); kb < split_begin(p, sp + 1); ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
                     const uint32_t buf = it % NBUF;
@@ -466,19 +538,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         TileCursor<BM, RASTER_GM> cur;
         cur.init(p);
         uint32_t it = 0;
-        auto make_tile = [&](int mt, int nt) {
+        auto make_tile = [&](int64_t item, int mt, int nt) {
+            const int sp = static_cast<int>(item % p.splits);
             return EpiTile{cur.row0 + int64_t(mt) * BM + r_in_tile, cur.row0 + cur.rows,
-                           int64_t(nt) * BN + h * EPI_COLS, cur.g};
+                           int64_t(nt) * BN + h * EPI_COLS, cur.g, split_begin(p, sp), split_begin(p, sp + 1),
+                           item / p.splits, sp};
         };
         int mt = 0, nt = 0;
-        int64_t t = blockIdx.x;
-        bool have = cur.seek(p, t, mt, nt);
-        EpiTile tile = have ? make_tile(mt, nt) : EpiTile{0, 0, 0, 0};
+        int64_t t = blockIdx.x;  // work item = tile * splits + split
+        bool have = cur.seek(p, t / p.splits, mt, nt);
+        EpiTile tile = have ? make_tile(t, mt, nt) : EpiTile{0, 0, 0, 0, 0, 0, 0, 0};
         ScalePre pre = prefetch_scales(p, tile);
         while (have) {
             const int64_t tn = t + gridDim.x;
-            const bool have_next = cur.seek(p, tn, mt, nt);
-            const EpiTile next = have_next ? make_tile(mt, nt) : tile;
+            const bool have_next = cur.seek(p, tn / p.splits, mt, nt);
+            const EpiTile next = have_next ? make_tile(tn, mt, nt) : tile;
             ScalePre next_pre = pre;
             promote_tile<BN, NBUF, false>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd, h,
                                           lane, tfull, tempty, it);
@@ -646,12 +720,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t it = 0;
         auto make_tile = [&](int mt, int nt) {
             return EpiTile{cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM + r_in_tile,
-                           cur.row0 + cur.rows, int64_t(nt) * PAIR_BN + h * EPI_COLS, cur.g};
+                           cur.row0 + cur.rows, int64_t(nt) * PAIR_BN + h * EPI_COLS, cur.g, 0, p.num_kb, 0, 0};
         };
         int mt = 0, nt = 0;
         int64_t t = pair;
         bool have = cur.seek(p, t, mt, nt);
-        EpiTile tile = have ? make_tile(mt, nt) : EpiTile{0, 0, 0, 0};
+        EpiTile tile = have ? make_tile(mt, nt) : EpiTile{0, 0, 0, 0, 0, 0, 0, 0};
         ScalePre pre = prefetch_scales(p, tile);
         while (have) {
             const int64_t tn = t + npairs;
@@ -726,6 +800,36 @@ cudaError_t device_info(int& sms) {
     }
     sms = di.sms;
     return cudaSuccess;
+}
+
+// Split-K plan for the one-CTA kernel (BN = 256) on small-M dense problems: choose S (slices
+// of the K loop per tile) minimising the busiest CTA's share ceil(tiles*S/sms)/S of one tile's
+// k-loop, ties to fewer slices; S = 1 when the tiles already fill the machine.
+int plan_splits(int64_t m, int64_t n, int64_t k, int sms) {
+    const int64_t tiles = ((m + BM - 1) / BM) * ((n + 255) / 256);
+    const int64_t num_kb = k / BK;
+    if (tiles <= 0 || tiles * 2 > sms || num_kb < 2) return 1;
+    // fp32 partials cost 8 B per output element and slice (write + read): keep them within
+    // half of the weight bytes (N*K) -> S <= K / (16 M)
+    const int64_t s_traffic = k / (16 * (m > 0 ? m : 1));
+    int best = 1;
+    double best_cost = 1e30;
+    for (int sp = 1; sp <= 16 && sp <= num_kb && sp <= s_traffic; ++sp) {
+        const double cost = static_cast<double>((tiles * sp + sms - 1) / sms) / sp;
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = sp;
+        }
+    }
+    return best;
+}
+// Workspace: [counters: SPLIT_COUNTER_BYTES][partials]; the counter region sits at a fixed
+// offset so the "left zeroed" invariant holds whatever shape used the workspace before.
+constexpr size_t SPLIT_COUNTER_BYTES = 4096;  // >= 4 B x the most tiles that ever split (sms / 2)
+size_t split_ws_bytes(int64_t m, int64_t n, int sp) {
+    if (sp <= 1) return 0;
+    const int64_t tiles = ((m + BM - 1) / BM) * ((n + 255) / 256);
+    return SPLIT_COUNTER_BYTES + static_cast<size_t>(tiles * sp * BM * 256) * 4;
 }
 
 // Kernel choice (see launch_cfg): env FP8Q_GEMM_KIND = 128 | 256 | 1128 | 1256 overrides (dev only).
@@ -807,6 +911,18 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
     p.num_n_tiles = static_cast<int>((a.n + BN - 1) / BN);
     p.offsets = a.offsets;
     p.groups = a.offsets != nullptr ? a.groups : 1;
+    p.splits = 1;
+    p.ws = nullptr;
+    p.counters = nullptr;
+    if (!kPair && KIND == 256 && a.offsets == nullptr) {
+        const int sp = plan_splits(a.m, a.n, a.k, sms);
+        const size_t need = split_ws_bytes(a.m, a.n, sp);
+        if (sp > 1 && a.workspace != nullptr && a.workspace_bytes >= need) {
+            p.splits = sp;
+            p.counters = static_cast<int32_t*>(a.workspace);
+            p.ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + SPLIT_COUNTER_BYTES);
+        }
+    }
 
     if (kPair) {
         int64_t clusters = sms / 2;
@@ -819,8 +935,8 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
     } else {
         int64_t grid = sms;
         if (a.offsets == nullptr) {
-            const int64_t tiles = ((a.m + BM - 1) / BM) * p.num_n_tiles;
-            grid = tiles < sms ? tiles : sms;
+            const int64_t items = ((a.m + BM - 1) / BM) * p.num_n_tiles * p.splits;
+            grid = items < sms ? items : sms;
         }
         fp8_block_gemm_kernel<BN><<<static_cast<unsigned>(grid), NUM_THREADS, Cfg<BN>::SMEM_BYTES, stream>>>(
             tmA, tmB, tmD, p);
@@ -831,6 +947,14 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
 }  // namespace
 
 void set_gemm_trace(uint32_t* dev_ptr) { g_trace = dev_ptr; }
+
+size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped) {
+    if (grouped || m <= 0 || n <= 0 || k <= 0) return 0;
+    int sms = 0;
+    if (device_info(sms) != cudaSuccess) sms = 148;
+    if (m >= 2 * BM) return 0;  // the CTA-pair kernel does not split K
+    return split_ws_bytes(m, n, plan_splits(m, n, k, sms));
+}
 
 cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* launches) {
     *launches = 0;

@@ -47,7 +47,12 @@ struct GemmArgs {
     int64_t m, n, k;
     const int32_t* offsets;  // device [groups + 1] or nullptr (dense)
     int32_t groups;
+    void* workspace;         // split-K workspace (zero-filled before first use), may be null
+    size_t workspace_bytes;
 };
+
+// Bytes of workspace with which launch_fp8_block_gemm uses split-K for this shape (0: never).
+size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped);
 
 // Enqueue the tcgen05 blockwise-scaled FP8 GEMM.  Returns cudaSuccess or the first error.
 cudaError_t launch_fp8_block_gemm(const GemmArgs& args, cudaStream_t stream, int* launches);

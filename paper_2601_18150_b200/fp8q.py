@@ -191,6 +191,21 @@ def _out(out, m, n, out_dtype, device):
     return out
 
 
+_WS: dict = {}
+
+
+def _workspace(device, stream_handle: int, nbytes: int):
+    """Zero-filled split-K workspace cached per (device, stream); the kernels leave it zeroed."""
+    if nbytes == 0:
+        return None, 0
+    key = (device.index, stream_handle)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws.data_ptr(), ws.numel()
+
+
 def fp8_block_gemm(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_scales: torch.Tensor,
                    out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None,
                    stream=None) -> torch.Tensor:
@@ -207,10 +222,13 @@ def fp8_block_gemm(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_s
     out = _out(out, m, n, out_dtype, a.device)
     ld_sa = a_scales.stride(0) if a_scales.shape[0] > 1 else a_scales.shape[1]
     ld_sb = b_scales.stride(0) if b_scales.shape[0] > 1 else b_scales.shape[1]
-    _check(load_library().fp8_block_gemm(
+    lib = load_library()
+    sh = _stream(stream)
+    ws_ptr, ws_bytes = _workspace(a.device, sh, int(lib.fp8_block_gemm_workspace_size(m, n, k)))
+    _check(lib.fp8_block_gemm(
         a.data_ptr(), _ld(a), a_scales.data_ptr(), ld_sa, b.data_ptr(), _ld(b), b_scales.data_ptr(),
         ld_sb, out.data_ptr(), _ld(out), FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16,
-        m, n, k, None, 0, _stream(stream)), "fp8_block_gemm")
+        m, n, k, ws_ptr, ws_bytes, sh), "fp8_block_gemm")
     return out
 
 

@@ -71,7 +71,7 @@ def test_validation_paths_without_gpu(lib):
     assert lib.fp8_block_gemm(fake, 136, fake, 4, fake, 128, fake, 1, fake, 16, 0, 4, 16, 128, None, 0, None) == 3
     assert lib.fp8_block_gemm_grouped(fake, 128, fake, 4, fake, 128, 2048, fake, 1, 1, fake, 16, 0,
                                       4, 16, 128, fake, -1, None, 0, None) == 2
-    assert lib.fp8_block_gemm_workspace_size(8192, 6144, 4096) == 0
+    assert lib.fp8_block_gemm_workspace_size(8192, 6144, 4096) == 0  # prefill: no split-K
 
 
 def test_product_package_never_imports_oracle():

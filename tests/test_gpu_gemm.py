@@ -165,13 +165,66 @@ def test_grouped_qwen3_30b_fc1_sampled(skew):
     assert rel_frobenius(got, ref) <= TOL
 
 
+def _run_unsplit(a, sa, b, sb):
+    """fp8_block_gemm through the C-ABI with no workspace (never splits K), F32 output."""
+    m, k = a.shape
+    n = b.shape[0]
+    lib = fp8q.load_library()
+    da = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    dsa = act_scales_mn_from_logical(sa, fp8q.act_scales_ld(m))
+    db = torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    dsb = torch.from_numpy(np.ascontiguousarray(sb)).cuda()
+    y = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    st = lib.fp8_block_gemm(da.data_ptr(), k, dsa.data_ptr(), dsa.stride(0), db.data_ptr(), k,
+                            dsb.data_ptr(), dsb.shape[1], y.data_ptr(), n, 1, m, n, k, None, 0,
+                            torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert st == 0
+    return y
+
+
 def test_grouped_equals_dense_per_group_bitwise():
-    # O8: grouped == per-group dense, and the kernel is deterministic -> bitwise equality
+    # O8: grouped == per-group dense (unsplit), and the kernel is deterministic -> bitwise
     sizes = [70, 0, 200, 9]
     a, sa, b, sb, off, y = _grouped_case(sizes, 256, 384, 7)
     for g in range(len(sizes)):
         r0, r1 = int(off[g]), int(off[g + 1])
         if r1 == r0:
             continue
-        yd = _run(a[r0:r1], sa[r0:r1], b[g], sb[g])
+        yd = _run_unsplit(a[r0:r1], sa[r0:r1], b[g], sb[g])
         assert torch.equal(yd.view(torch.int32), y[r0:r1].contiguous().view(torch.int32))
+
+
+@pytest.mark.parametrize("m,n,k", [(64, 4096, 4096), (1, 6144, 4096), (200, 4096, 12288)])
+def test_gemm_splitk_decode(m, n, k):
+    # small M: the binding passes a workspace, the kernel splits K; the last slice of each tile
+    # sums the slices in slice order -> deterministic; the workspace is left zeroed (reusable)
+    lib = fp8q.load_library()
+    assert lib.fp8_block_gemm_workspace_size(m, n, k) > 0
+    a, sa, b, sb = _operands(m, n, k, 31)
+    y1 = _run(a, sa, b, sb)
+    y2 = _run(a, sa, b, sb)
+    assert torch.equal(y1.view(torch.int32), y2.view(torch.int32))
+    ref = oracle.gemm_rows(a, sa, b, sb, np.arange(min(m, 16)))
+    assert rel_frobenius(y1[:min(m, 16)].cpu().numpy(), ref) <= 1e-5
+    # the same problem without a workspace runs unsplit: equal up to fp32 summation order
+    da = torch.from_numpy(a).cuda()
+    dsa = act_scales_mn_from_logical(sa, fp8q.act_scales_ld(m))
+    yu = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    st = lib.fp8_block_gemm(da.data_ptr(), k, dsa.data_ptr(), dsa.stride(0),
+                            torch.from_numpy(b).cuda().data_ptr(), k,
+                            torch.from_numpy(sb).cuda().data_ptr(), sb.shape[1], yu.data_ptr(), n, 1,
+                            m, n, k, None, 0, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert st == 0
+    assert rel_frobenius(y1.cpu().numpy(), yu.cpu().numpy()) <= 1e-6
+
+
+def test_splitk_workspace_reused_across_shapes():
+    # the cached workspace is shared by GEMMs of different shapes: its counters must always be
+    # found zeroed (regression: counters once lived after the shape-dependent partials)
+    cases = [(64, 4096, 4096), (8, 6144, 4096), (64, 4096, 4096), (1, 4096, 12288), (8, 6144, 4096)]
+    for i, (m, n, k) in enumerate(cases):
+        a, sa, b, sb = _operands(m, n, k, 40 + i)
+        y = _run(a, sa, b, sb).cpu().numpy()
+        assert rel_frobenius(y, oracle.gemm_rows(a, sa, b, sb)) <= 1e-5, (m, n, k)
