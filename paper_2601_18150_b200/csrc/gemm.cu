@@ -110,18 +110,20 @@ __device__ __forceinline__ void trace_ev(const KParams& p, uint32_t it, int ev) 
 // tile (128 for one CTA, 256 for a CTA pair), GM = m-tiles per raster band.
 template <int TM, int GM>
 struct TileCursor {
+    // 32-bit tile arithmetic on purpose: 64-bit division is a ~100-instruction software
+    // routine, and this runs between tiles on the promotion warps' critical path.
     int g;
-    int64_t base;   // first linear tile index of group g
-    int64_t row0;   // first A/D row of group g
-    int64_t rows;   // rows in group g
-    int64_t mtiles; // ceil(rows / BM)
+    int base;    // first linear tile index of group g
+    int row0;    // first A/D row of group g
+    int rows;    // rows in group g
+    int mtiles;  // ceil(rows / TM)
     __device__ void load(const KParams& p) {
         if (p.offsets != nullptr) {
             row0 = p.offsets[g];
-            rows = static_cast<int64_t>(p.offsets[g + 1]) - row0;
+            rows = p.offsets[g + 1] - row0;
         } else {
             row0 = 0;
-            rows = p.m;
+            rows = static_cast<int>(p.m);
         }
         mtiles = (rows + TM - 1) / TM;
     }
@@ -131,7 +133,7 @@ struct TileCursor {
         if (p.groups > 0) load(p);
     }
     // Returns false when t is past the last tile.
-    __device__ bool seek(const KParams& p, int64_t t, int& mt, int& nt) {
+    __device__ bool seek(const KParams& p, int t, int& mt, int& nt) {
         if (g >= p.groups) return false;
         while (t >= base + mtiles * p.num_n_tiles) {
             base += mtiles * p.num_n_tiles;
@@ -141,12 +143,14 @@ struct TileCursor {
         // Grouped raster: bands of GM m-tiles; inside a band m is fastest, so the ~148
         // concurrent tiles cover a compact RASTER_GM x ~9 block of the output and both the A
         // band and the B tiles they touch stay L2-resident (K = 12288 would otherwise re-read A).
-        const int64_t l = t - base;
-        const int64_t band = l / (int64_t(GM) * p.num_n_tiles);
-        const int64_t r = l - band * (int64_t(GM) * p.num_n_tiles);
-        const int64_t gm = min(int64_t(GM), mtiles - band * GM);
-        mt = static_cast<int>(band * GM + r % gm);
-        nt = static_cast<int>(r / gm);
+        const unsigned l = static_cast<unsigned>(t - base);
+        const unsigned span = static_cast<unsigned>(GM * p.num_n_tiles);
+        const unsigned band = l / span;
+        const unsigned r = l - band * span;
+        const unsigned gm = min(static_cast<unsigned>(GM), static_cast<unsigned>(mtiles) - band * GM);
+        const unsigned q = r / gm;
+        mt = static_cast<int>(band * GM + (r - q * gm));
+        nt = static_cast<int>(q);
         return true;
     }
 };
@@ -217,7 +221,7 @@ __device__ __forceinline__ ScalePre prefetch_scales(const KParams& p, const EpiT
 }
 
 __device__ __forceinline__ int split_begin(const KParams& p, int s) {
-    return static_cast<int>((static_cast<int64_t>(s) * p.num_kb) / p.splits);
+    return (s * p.num_kb) / p.splits;  // 32-bit: s * num_kb < 2^31 for any real K
 }
 
 // For every k-block: wait for the partial in TMEM buffer it % NBUF, tcgen05.ld it, hand the
@@ -232,6 +236,7 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
     constexpr int EPI_COLS = BN / 2;
     constexpr int CHUNKS = EPI_COLS / 32;  // tcgen05.ld 32x32b.x32 per promotion thread
     static_assert(EPI_COLS / 32 <= EPI_CHUNKS, "BF16 row segment must fit the staging chunks");
+    if (threadIdx.x == EPI_WARP0 * 32) trace_ev(p, it, 4);  // dev timeline: tile entry
     const int64_t row = tile.row;
     const int64_t row_end = tile.row_end;
     const int64_t col0 = tile.col0;
@@ -477,9 +482,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
-            for (int64_t item = blockIdx.x;; item += gridDim.x) {
-                if (!cur.seek(p, item / p.splits, mt, nt)) break;
-                const int sp = static_cast<int>(item % p.splits);
+            for (int item = blockIdx.x;; item += gridDim.x) {
+                const int tq = item / p.splits;
+                if (!cur.seek(p, tq, mt, nt)) break;
+                const int sp = item - tq * p.splits;
                 const int32_t arow = static_cast<int32_t>(cur.row0 + int64_t(mt) * BM);
                 const int32_t brow = nt * BN;
                 for (int kb = split_begin(p, sp); kb < split_begin(p, sp + 1); ++kb, ++it) {
@@ -502,9 +508,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
-            for (int64_t item = blockIdx.x;; item += gridDim.x) {
-                if (!cur.seek(p, item / p.splits, mt, nt)) break;
-                const int sp = static_cast<int>(item % p.splits);
+            for (int item = blockIdx.x;; item += gridDim.x) {
+                const int tq = item / p.splits;
+                if (!cur.seek(p, tq, mt, nt)) break;
+                const int sp = item - tq * p.splits;
                 for (int kb = split_begin(p, sp); kb < split_begin(p, sp + 1); ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
@@ -538,19 +545,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         TileCursor<BM, RASTER_GM> cur;
         cur.init(p);
         uint32_t it = 0;
-        auto make_tile = [&](int64_t item, int mt, int nt) {
-            const int sp = static_cast<int>(item % p.splits);
-            return EpiTile{cur.row0 + int64_t(mt) * BM + r_in_tile, cur.row0 + cur.rows,
+        auto make_tile = [&](int item, int mt, int nt) {
+            const int tq = item / p.splits;
+            const int sp = item - tq * p.splits;
+            return EpiTile{cur.row0 + int64_t(mt) * BM + r_in_tile, int64_t(cur.row0) + cur.rows,
                            int64_t(nt) * BN + h * EPI_COLS, cur.g, split_begin(p, sp), split_begin(p, sp + 1),
-                           item / p.splits, sp};
+                           tq, sp};
         };
         int mt = 0, nt = 0;
-        int64_t t = blockIdx.x;  // work item = tile * splits + split
+        int t = blockIdx.x;  // work item = tile * splits + split
         bool have = cur.seek(p, t / p.splits, mt, nt);
         EpiTile tile = have ? make_tile(t, mt, nt) : EpiTile{0, 0, 0, 0, 0, 0, 0, 0};
         ScalePre pre = prefetch_scales(p, tile);
         while (have) {
-            const int64_t tn = t + gridDim.x;
+            const int tn = t + gridDim.x;
             const bool have_next = cur.seek(p, tn / p.splits, mt, nt);
             const EpiTile next = have_next ? make_tile(tn, mt, nt) : tile;
             ScalePre next_pre = pre;
@@ -654,7 +662,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
-            for (int64_t t = pair; cur.seek(p, t, mt, nt); t += npairs) {
+            for (int t = static_cast<int>(pair); cur.seek(p, t, mt, nt); t += static_cast<int>(npairs)) {
                 const int32_t arow = static_cast<int32_t>(cur.row0 + int64_t(mt) * 2 * BM + rank * BM);
                 const int32_t brow = nt * PAIR_BN + static_cast<int32_t>(rank) * PAIR_B_HALF;
                 for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
@@ -679,7 +687,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
-            for (int64_t t = pair; cur.seek(p, t, mt, nt); t += npairs) {
+            for (int t = static_cast<int>(pair); cur.seek(p, t, mt, nt); t += static_cast<int>(npairs)) {
                 for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
@@ -720,15 +728,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t it = 0;
         auto make_tile = [&](int mt, int nt) {
             return EpiTile{cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM + r_in_tile,
-                           cur.row0 + cur.rows, int64_t(nt) * PAIR_BN + h * EPI_COLS, cur.g, 0, p.num_kb, 0, 0};
+                           int64_t(cur.row0) + cur.rows, int64_t(nt) * PAIR_BN + h * EPI_COLS, cur.g, 0, p.num_kb,
+                           0, 0};
         };
         int mt = 0, nt = 0;
-        int64_t t = pair;
+        int t = static_cast<int>(pair);
         bool have = cur.seek(p, t, mt, nt);
         EpiTile tile = have ? make_tile(mt, nt) : EpiTile{0, 0, 0, 0, 0, 0, 0, 0};
         ScalePre pre = prefetch_scales(p, tile);
         while (have) {
-            const int64_t tn = t + npairs;
+            const int tn = t + static_cast<int>(npairs);
             const bool have_next = cur.seek(p, tn, mt, nt);
             const EpiTile next = have_next ? make_tile(mt, nt) : tile;
             ScalePre next_pre = pre;

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Dev tool: print CTA 0's pipeline timeline (SM clock) for one fp8_block_gemm launch.
 Events per k-block: 0 producer issue, 1 MMA sees TMEM buffer free, 2 MMA issue (smem full),
-3 promotion sees partial ready, (4 unused), 5 promotion done, 6/7 store begin/end."""
+3 promotion sees partial ready, 4 promotion tile entry (first k-block of a tile only), 5 promotion done, 6/7 store begin/end."""
 import ctypes
 import os
 import sys
