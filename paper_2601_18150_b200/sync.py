@@ -143,39 +143,63 @@ class WeightSyncEngine:
         h2 = dist.all_gather_into_tensor(s, s[sh.srow0:sh.srow1], group=self.group, async_op=async_op)
         return [h for h in (h1, h2) if h is not None]
 
-    def sync_step(self, step: int, shards: Dict[str, torch.Tensor], comm_stream=None) -> None:
+    def gather_many(self, names: Sequence[str]) -> None:
+        """All-gathers of several tensors as ONE grouped NCCL call (one launch for the whole
+        bucket instead of two per tensor); backends without coalescing (gloo) loop."""
+        if self.world == 1 or not names:
+            return
+        backend = dist.get_backend(self.group)
+        if backend == "nccl":
+            with dist._coalescing_manager(group=self.group, device=self.device):
+                for n in names:
+                    self.gather(n)
+        else:
+            for n in names:
+                self.gather(n)
+
+    def _local_items(self, specs, shards):
+        items = []
+        for s in specs:
+            sh = self.my_shard(s.name)
+            w = shards[s.name]
+            if w.shape[0] != sh.row1 - sh.row0:
+                raise ValueError(f"{s.name}: shard has {w.shape[0]} rows, plan says {sh.row1 - sh.row0}")
+            items.append((w, self.codes[s.name][sh.row0:sh.row1], self.scales[s.name][sh.srow0:sh.srow1]))
+        return items
+
+    def sync_step(self, step: int, shards: Dict[str, torch.Tensor], comm_stream=None,
+                  bucket: int = 16) -> None:
         """One weight synchronisation: quantize every local shard, all-gather.
-        With a comm stream, tensor i's gather overlaps tensor i+1's quantization."""
+
+        Buckets of `bucket` tensors: one batched quantizer launch per bucket, then one grouped
+        all-gather of that bucket -- on `comm_stream` when given, so bucket i's gather overlaps
+        bucket i+1's quantization on the compute stream."""
         if step <= self.loaded_step:
             raise StaleStepError(f"step {step} is not newer than loaded step {self.loaded_step}")
         missing = [s.name for s in self.specs if s.name not in shards]
         if missing:
             raise KeyError(f"missing shards: {missing}")
-        if self.quantize_fn is _default_quantize and (comm_stream is None or self.world == 1):
-            # one batched launch for every local shard (the whole layer's weights)
+        batched = self.quantize_fn is _default_quantize
+        if batched:
             from .fp8q import quantize_weight_blockwise_batched
-            items = []
-            for s in self.specs:
-                sh = self.my_shard(s.name)
-                w = shards[s.name]
-                if w.shape[0] != sh.row1 - sh.row0:
-                    raise ValueError(f"{s.name}: shard has {w.shape[0]} rows, plan says {sh.row1 - sh.row0}")
-                items.append((w, self.codes[s.name][sh.row0:sh.row1], self.scales[s.name][sh.srow0:sh.srow1]))
-            quantize_weight_blockwise_batched(items)
-            for s in self.specs:
-                self.gather(s.name)
-        elif comm_stream is None or self.world == 1:
-            for s in self.specs:
-                self.quantize_local(s.name, shards[s.name])
-                self.gather(s.name)
-        else:
-            compute = torch.cuda.current_stream(self.device)
-            for s in self.specs:
-                self.quantize_local(s.name, shards[s.name])
+        overlap = comm_stream is not None and self.world > 1
+        compute = torch.cuda.current_stream(self.device) if overlap else None
+        for b0 in range(0, len(self.specs), bucket):
+            chunk = self.specs[b0:b0 + bucket]
+            if batched:
+                quantize_weight_blockwise_batched(self._local_items(chunk, shards))
+            else:
+                for s in chunk:
+                    self.quantize_local(s.name, shards[s.name])
+            names = [s.name for s in chunk]
+            if overlap:
                 ev = torch.cuda.Event()
                 ev.record(compute)
                 with torch.cuda.stream(comm_stream):
                     comm_stream.wait_event(ev)
-                    self.gather(s.name)
+                    self.gather_many(names)
+            else:
+                self.gather_many(names)
+        if overlap:
             compute.wait_stream(comm_stream)
         self.loaded_step = step
