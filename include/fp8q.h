@@ -178,7 +178,7 @@ int64_t fp8q_kernel_launches(void);
  * fp8q_debug_set_gemm_trace -- DEVELOPMENT ONLY.  When dev_ptr (device, >= 96*8 uint32) is
  * non-NULL, later fp8_block_gemm launches make CTA 0 write SM clock() stamps of its first 96
  * k-blocks' pipeline events (producer issue, MMA tmem-free / smem-full, promotion
- * partial-ready / release / done) to dev_ptr[kblock*8 + event].  NULL disables.  Not
+ * partial-ready / release / done) to dev_ptr[kblock*12 + event].  NULL disables.  Not
  * thread-safe; never set in production.
  */
 void fp8q_debug_set_gemm_trace(uint32_t* dev_ptr);

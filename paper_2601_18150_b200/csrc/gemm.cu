@@ -31,6 +31,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "ptx.cuh"
 #include "quant_kernels.h"
@@ -100,7 +101,7 @@ struct KParams {
 
 // Dev-only timeline: CTA 0 records clock() at pipeline events of its first TRACE_KB k-blocks.
 constexpr int TRACE_KB = 96;
-constexpr int TRACE_EV = 8;
+constexpr int TRACE_EV = 12;
 __device__ __forceinline__ void trace_ev(const KParams& p, uint32_t it, int ev) {
     if (p.trace != nullptr && blockIdx.x == 0 && it < TRACE_KB)
         p.trace[it * TRACE_EV + ev] = static_cast<uint32_t>(clock64());
@@ -232,7 +233,8 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
                                              const EpiTile& tile, const ScalePre& pre, bool has_next,
                                              const EpiTile& next, ScalePre& next_pre, uint32_t tmem,
                                              int qd, int h, int lane, uint64_t* tfull,
-                                             uint64_t* tempty, uint32_t& it) {
+                                             uint64_t* tempty, uint32_t& it, uint64_t* stg_full,
+                                             uint64_t* stg_empty, uint32_t& tile_no) {
     constexpr int EPI_COLS = BN / 2;
     constexpr int CHUNKS = EPI_COLS / 32;  // tcgen05.ld 32x32b.x32 per promotion thread
     static_assert(EPI_COLS / 32 <= EPI_CHUNKS, "BF16 row segment must fit the staging chunks");
@@ -344,90 +346,142 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
         if (threadIdx.x == EPI_WARP0 * 32) p.counters[tile.tile] = 0;  // reusable workspace
     }
     if (col0 >= p.n) return;  // warp-uniform: these columns are past the matrix
-    // ---- output: the warp's 32 rows x EPI_COLS columns.  Full 32-row slices go through
-    // swizzled smem chunks (32 rows x 64 B) and asynchronous TMA stores (the tensor map clips
-    // at m and n); a slice that straddles the end of a MoE group (rows past it belong to the
-    // next group) is written with masked direct stores instead.
+    // ---- output: the warp's 32 rows x EPI_COLS columns, through the warp's smem staging:
+    // each lane writes its row as 64-byte-swizzled 16 B units (conflict-free), then the warp
+    // reads the staging back row-contiguously so every STG.128 instruction writes two full
+    // 256-byte row segments (coalesced; rows past row_end and columns past n are masked, which
+    // also covers MoE group tails).  Plain loads/stores: no async-proxy fence, no TMA queue.
+    (void)tmD;
     const int64_t row_base = row - lane;
-    if (row_base + 32 <= row_end || p.offsets == nullptr) {
+    if (!p.out_f32 && p.splits == 1 && EPI_COLS * 2 == 4 * 64) {  // must match the store-warp role
+        // BF16 production path: park the row segment in this warp's staging (64-byte swizzled
+        // 16 B units, conflict-free) and hand it to the store warp of this column half, which
+        // writes it to global memory while this warp already promotes the next tile.
+        const uint32_t ph = tile_no & 1u;
+        ++tile_no;
+        mbar_wait(&stg_empty[h], ph ^ 1u);  // the store warp drained this staging (a tile ago)
         const uint32_t swz = static_cast<uint32_t>((lane >> 1) & 3);
-        if (p.out_f32) {
+        const uint32_t stg_base = smem_u32(stg);
 #pragma unroll
-            for (int c = 0; c < EPI_COLS / 16; ++c) {
-                uint8_t* sb = stg + (c % EPI_CHUNKS) * EPI_CHUNK_BYTES;
-                if (lane == 0) bulk_wait_group_read<EPI_CHUNKS - 1>();
-                __syncwarp();
-                const uint32_t base = smem_u32(sb) + lane * 64;
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t base = stg_base + c * EPI_CHUNK_BYTES + lane * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 a = acc[c * 16 + j * 4 + e];
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(a.x, a.y);
+                    w[e] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                st_shared_v4(base + 16u * (static_cast<uint32_t>(j) ^ swz), w[0], w[1], w[2], w[3]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&stg_full[h]);  // release: the staging writes above
+        if (tr_store) trace_ev(p, it - 1, 7);
+        return;
+    }
+    const uint32_t swz = static_cast<uint32_t>((lane >> 1) & 3);
+    const uint32_t stg_base = smem_u32(stg);
+    // One staging pass: CH chunks of 32 rows x 64 B (CH = 4 -> 256 B row segments, 16 lanes
+    // per row; CH = 2 -> 128 B, 8 lanes per row).
+    auto drain = [&](int64_t gcol0_bytes, int esz, auto ch_tag) {
+        constexpr int CH = decltype(ch_tag)::value;
+        constexpr int UPR = CH * 4;        // 16 B units per row segment
+        constexpr int RPI = 32 / UPR;      // rows per warp instruction
+        __syncwarp();
+        char* dbase = static_cast<char*>(p.d);
+#pragma unroll
+        for (int i = 0; i < 32 / RPI; ++i) {
+            const int r = RPI * i + lane / UPR;
+            const int u = lane % UPR;
+            const uint32_t src = stg_base + (u >> 2) * EPI_CHUNK_BYTES + r * 64 +
+                                 16u * (static_cast<uint32_t>(u & 3) ^ static_cast<uint32_t>((r >> 1) & 3));
+            uint32_t x0, x1, x2, x3;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(src));
+            const int64_t grow = row_base + r;
+            const int64_t gbyte = gcol0_bytes + 16 * u;
+            if (grow < row_end && gbyte < p.n * esz)
+                st_v4(dbase + grow * p.ld_d * esz + gbyte, x0, x1, x2, x3);
+        }
+        __syncwarp();
+    };
+    if (p.out_f32) {
+        constexpr int CH = EPI_COLS * 4 >= 256 ? 4 : 2;  // chunks per pass
+        constexpr int PASS_COLS = CH * 16;               // fp32 columns per pass
+#pragma unroll
+        for (int pass = 0; pass < EPI_COLS / PASS_COLS; ++pass) {
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const uint32_t base = stg_base + c * EPI_CHUNK_BYTES + lane * 64;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const float2 a0 = acc[c * 8 + j * 2], a1 = acc[c * 8 + j * 2 + 1];
-                    st_shared_v4(base + 16u * (static_cast<uint32_t>(j) ^ swz), __float_as_uint(a0.x),
-                                 __float_as_uint(a0.y), __float_as_uint(a1.x), __float_as_uint(a1.y));
-                }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_2d(tmD, sb, static_cast<int32_t>(col0 + c * 16), static_cast<int32_t>(row_base));
-                    bulk_commit_group();
+                    const int a = pass * (PASS_COLS / 2) + c * 8 + j * 2;
+                    st_shared_v4(base + 16u * (static_cast<uint32_t>(j) ^ swz), __float_as_uint(acc[a].x),
+                                 __float_as_uint(acc[a].y), __float_as_uint(acc[a + 1].x),
+                                 __float_as_uint(acc[a + 1].y));
                 }
             }
-        } else {
-            // BF16: the thread's 128 columns are exactly EPI_CHUNKS chunks -> write them all,
-            // one async-proxy fence, then the chunk stores.
-            if (lane == 0) bulk_wait_group_read<0>();  // previous tile's stores left the chunks
-            __syncwarp();
+            drain((col0 + pass * PASS_COLS) * 4, 4, std::integral_constant<int, CH>{});
+        }
+    } else {
+        constexpr int CH = EPI_COLS * 2 >= 256 ? 4 : 2;
+        constexpr int PASS_COLS = CH * 32;  // bf16 columns per pass
 #pragma unroll
-            for (int c = 0; c < EPI_COLS / 32; ++c) {
-                const uint32_t base = smem_u32(stg + c * EPI_CHUNK_BYTES) + lane * 64;
+        for (int pass = 0; pass < EPI_COLS / PASS_COLS; ++pass) {
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const uint32_t base = stg_base + c * EPI_CHUNK_BYTES + lane * 64;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     uint32_t w[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const float2 a = acc[c * 16 + j * 4 + e];
+                        const float2 a = acc[pass * (PASS_COLS / 2) + c * 16 + j * 4 + e];
                         __nv_bfloat162 b2 = __floats2bfloat162_rn(a.x, a.y);
                         w[e] = *reinterpret_cast<uint32_t*>(&b2);
                     }
                     st_shared_v4(base + 16u * (static_cast<uint32_t>(j) ^ swz), w[0], w[1], w[2], w[3]);
                 }
             }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-#pragma unroll
-                for (int c = 0; c < EPI_COLS / 32; ++c)
-                    tma_store_2d(tmD, stg + c * EPI_CHUNK_BYTES, static_cast<int32_t>(col0 + c * 32),
-                                 static_cast<int32_t>(row_base));
-                bulk_commit_group();
-            }
-        }
-        if (tr_store) trace_ev(p, it - 1, 7);
-        return;
-    }
-    if (!live) return;
-    if (p.out_f32) {
-        float* drow = static_cast<float*>(p.d) + row * p.ld_d + col0;
-#pragma unroll
-        for (int j = 0; j < EPI_COLS / 4; ++j) {
-            if (col0 + j * 4 < p.n)
-                st_v4(drow + j * 4, __float_as_uint(acc[2 * j].x), __float_as_uint(acc[2 * j].y),
-                      __float_as_uint(acc[2 * j + 1].x), __float_as_uint(acc[2 * j + 1].y));
-        }
-    } else {
-        __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.d) + row * p.ld_d + col0;
-#pragma unroll
-        for (int j = 0; j < EPI_COLS / 8; ++j) {
-            if (col0 + j * 8 < p.n) {
-                uint32_t w[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[4 * j + e].x, acc[4 * j + e].y);
-                    w[e] = *reinterpret_cast<uint32_t*>(&b2);
-                }
-                st_v4(drow + j * 8, w[0], w[1], w[2], w[3]);
-            }
+            drain((col0 + pass * PASS_COLS) * 2, 2, std::integral_constant<int, CH>{});
         }
     }
+    if (tr_store) trace_ev(p, it - 1, 7);
+}
+
+// Store warp (warps 2 and 3, otherwise idle): for every tile, wait until the 4 promotion
+// warps of column half h have parked their 32 x 128 BF16 slices, copy the 4 slices to global
+// memory with coalesced STG.128 (two full 256-byte row segments per instruction; rows past
+// row_end / columns past n masked), then release the staging.
+__device__ __forceinline__ void store_tile_half(const KParams& p, const uint8_t* smEpi, int h, int lane,
+                                                int64_t row0_tile, int64_t row_end, int64_t col0,
+                                                uint64_t* stg_full, uint64_t* stg_empty, uint32_t& tile_no) {
+    const uint32_t ph = tile_no & 1u;
+    ++tile_no;
+    mbar_wait(&stg_full[h], ph);
+    char* dbase = static_cast<char*>(p.d);
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {  // slice of promotion warp EPI_WARP0 + 4h + q (TMEM quarter q)
+        const uint32_t sbase = smem_u32(smEpi + (4 * h + q) * EPI_CHUNKS * EPI_CHUNK_BYTES);
+        const int64_t rbase = row0_tile + q * 32;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int r = 2 * i + (lane >> 4);
+            const int u = lane & 15;
+            const uint32_t src = sbase + (u >> 2) * EPI_CHUNK_BYTES + r * 64 +
+                                 16u * (static_cast<uint32_t>(u & 3) ^ static_cast<uint32_t>((r >> 1) & 3));
+            uint32_t x0, x1, x2, x3;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(src));
+            const int64_t grow = rbase + r;
+            const int64_t gcol = col0 + 8 * u;
+            if (grow < row_end && gcol < p.n)
+                st_v4(dbase + (grow * p.ld_d + gcol) * 2, x0, x1, x2, x3);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&stg_empty[h]);
 }
 
 template <int BN_>
@@ -450,7 +504,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + NBUF;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+    uint64_t* stg_full = tempty + NBUF;   // [2]: per column half, 4 promotion warps arrive
+    uint64_t* stg_empty = stg_full + 2;   // [2]: the store warp of that half arrives
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -463,6 +519,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], NUM_EPI_WARPS);
+        }
+        for (int hh = 0; hh < 2; ++hh) {
+            mbar_init(&stg_full[hh], 4);
+            mbar_init(&stg_empty[hh], 1);
         }
         fence_mbar_init();
     }
@@ -534,6 +594,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
         }
+    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128) {
+        // ------------------------------------------------------------ store warps (BF16)
+        const int h = warp - 2;
+        TileCursor<BM, RASTER_GM> cur;
+        cur.init(p);
+        uint32_t tile_no = 0;
+        int mt, nt;
+        for (int t = blockIdx.x; cur.seek(p, t, mt, nt); t += gridDim.x) {
+            const int64_t col0 = int64_t(nt) * BN + h * EPI_COLS;
+            if (col0 >= p.n) {  // the promotion warps skip such halves too
+                continue;
+            }
+            store_tile_half(p, smEpi, h, lane, cur.row0 + int64_t(mt) * BM, int64_t(cur.row0) + cur.rows, col0,
+                            stg_full, stg_empty, tile_no);
+        }
     } else if (warp >= EPI_WARP0) {
         // ---------------------------------------------------------------- promotion warps
         regs_inc<REGS_EPI>();
@@ -541,10 +616,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int qd = warp & 3;                // TMEM lane quarter this warp may access
         const int r_in_tile = qd * 32 + lane;
         uint8_t* stg = smEpi + (warp - EPI_WARP0) * EPI_CHUNKS * EPI_CHUNK_BYTES;
+        if (lane == 0) tma_prefetch_desc(&tmD);
         const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
         TileCursor<BM, RASTER_GM> cur;
         cur.init(p);
         uint32_t it = 0;
+        uint32_t tile_no = 0;
         auto make_tile = [&](int item, int mt, int nt) {
             const int tq = item / p.splits;
             const int sp = item - tq * p.splits;
@@ -563,7 +640,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const EpiTile next = have_next ? make_tile(tn, mt, nt) : tile;
             ScalePre next_pre = pre;
             promote_tile<BN, NBUF, false>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd, h,
-                                          lane, tfull, tempty, it);
+                                          lane, tfull, tempty, it, stg_full, stg_empty, tile_no);
             tile = next;
             pre = next_pre;
             t = tn;
@@ -625,7 +702,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + NBUF;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+    uint64_t* stg_full = tempty + NBUF;
+    uint64_t* stg_empty = stg_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -642,6 +721,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);                  // multicast commit
             mbar_init(&tempty[b], 2 * NUM_EPI_WARPS);  // leader: promotion warps of both CTAs
+        }
+        for (int hh = 0; hh < 2; ++hh) {
+            mbar_init(&stg_full[hh], 4);
+            mbar_init(&stg_empty[hh], 1);
         }
         fence_mbar_init();
     }
@@ -715,6 +798,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 mbar_wait(&tempty[i % NBUF], (i / NBUF) & 1u);
             }
         }
+    } else if ((warp == 2 || warp == 3) && !p.out_f32) {
+        // ------------------------------------------------------------ store warps (BF16)
+        const int h = warp - 2;
+        TileCursor<2 * BM, PAIR_RASTER_GM> cur;
+        cur.init(p);
+        uint32_t tile_no = 0;
+        int mt, nt;
+        for (int t = static_cast<int>(pair); cur.seek(p, t, mt, nt); t += static_cast<int>(npairs)) {
+            const int64_t col0 = int64_t(nt) * PAIR_BN + h * EPI_COLS;
+            if (col0 >= p.n) continue;
+            store_tile_half(p, smEpi, h, lane, cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM,
+                            int64_t(cur.row0) + cur.rows, col0, stg_full, stg_empty, tile_no);
+        }
     } else if (warp >= EPI_WARP0) {
         // ---------------------------------------------------------------- promotion warps
         regs_inc<REGS_EPI>();
@@ -722,10 +818,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int qd = warp & 3;
         const int r_in_tile = qd * 32 + lane;
         uint8_t* stg = smEpi + (warp - EPI_WARP0) * EPI_CHUNKS * EPI_CHUNK_BYTES;
+        if (lane == 0) tma_prefetch_desc(&tmD);
         const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
         TileCursor<2 * BM, PAIR_RASTER_GM> cur;
         cur.init(p);
         uint32_t it = 0;
+        uint32_t tile_no = 0;
         auto make_tile = [&](int mt, int nt) {
             return EpiTile{cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM + r_in_tile,
                            int64_t(cur.row0) + cur.rows, int64_t(nt) * PAIR_BN + h * EPI_COLS, cur.g, 0, p.num_kb,
@@ -742,7 +840,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const EpiTile next = have_next ? make_tile(mt, nt) : tile;
             ScalePre next_pre = pre;
             promote_tile<PAIR_BN, NBUF, true>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd,
-                                              h, lane, tfull, tempty, it);
+                                              h, lane, tfull, tempty, it, stg_full, stg_empty, tile_no);
             tile = next;
             pre = next_pre;
             t = tn;

@@ -57,7 +57,7 @@ size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped);
 // Enqueue the tcgen05 blockwise-scaled FP8 GEMM.  Returns cudaSuccess or the first error.
 cudaError_t launch_fp8_block_gemm(const GemmArgs& args, cudaStream_t stream, int* launches);
 
-// Dev-only: record a pipeline timeline of CTA 0 into dev_ptr (96 k-blocks x 8 uint32 clocks).
+// Dev-only: record a pipeline timeline of CTA 0 into dev_ptr (96 k-blocks x 12 uint32 clocks).
 void set_gemm_trace(uint32_t* dev_ptr);
 
 }  // namespace fp8q

@@ -22,21 +22,21 @@ wq, ws = fp8q.quantize_weight_blockwise(w)
 xq, xs = fp8q.quantize_act_per_token_group(x)
 lib = fp8q.load_library()
 lib.fp8q_debug_set_gemm_trace.argtypes = [ctypes.c_void_p]
-tr = torch.zeros(96 * 8, dtype=torch.int32, device=dev)
+tr = torch.zeros(96 * 12, dtype=torch.int32, device=dev)
 for _ in range(3):
     fp8q.fp8_block_gemm(xq, xs, wq, ws)
 lib.fp8q_debug_set_gemm_trace(tr.data_ptr())
 fp8q.fp8_block_gemm(xq, xs, wq, ws)
 torch.cuda.synchronize()
 lib.fp8q_debug_set_gemm_trace(None)
-t = tr.cpu().numpy().view(np.uint32).reshape(96, 8).astype(np.int64)
+t = tr.cpu().numpy().view(np.uint32).reshape(96, 12).astype(np.int64)
 base = t[0, 0]
 t = (t - base) % (1 << 32)
-names = ["prod", "mma_tfree", "mma_issue", "epi_ready", "epi_rel", "epi_done", "st_begin", "st_end"]
+names = ["prod", "mma_tfree", "mma_issue", "epi_ready", "epi_entry", "epi_done", "st_begin", "st_end", "st_waited", "st_written", "st_fenced"]
 print("kb  " + " ".join(f"{n_:>10s}" for n_ in names) + "   d_issue  rdy-iss  rel-rdy  done-rdy")
 prev = None
 for i in range(96):
-    row = t[i, :8]
+    row = t[i, :11]
     d_issue = row[2] - prev if prev is not None else 0
     prev = row[2]
     print(f"{i:3d} " + " ".join(f"{v:10d}" for v in row)
