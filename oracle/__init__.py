@@ -58,6 +58,12 @@ def _load():
             lib.oracle_quantize_act_per_token_group.restype = ctypes.c_int
             lib.oracle_gemm_rows.argtypes = [P, I64, P, I64, P, I64, P, I64, I64, I64, P, I64, P, ctypes.c_int]
             lib.oracle_gemm_rows.restype = ctypes.c_int
+            lib.oracle_f64_to_bf16.argtypes = [ctypes.c_double]
+            lib.oracle_f64_to_bf16.restype = ctypes.c_uint16
+            lib.oracle_rmsnorm_bf16.argtypes = [P, I64, I64, P, ctypes.c_double, P]
+            lib.oracle_rmsnorm_bf16.restype = None
+            lib.oracle_silu_mul_bf16.argtypes = [P, I64, I64, P]
+            lib.oracle_silu_mul_bf16.restype = None
             _lib = lib
     return _lib
 
@@ -186,3 +192,44 @@ def gemm_grouped_rows(a_codes, a_scales, b_codes, b_scales, offsets, rows=None, 
         sel = np.nonzero(grp == g)[0]
         out[sel] = gemm_rows(a_codes, a_scales, b_codes[g], b_scales[g], rows[sel], nthreads)
     return out
+
+
+# ---------------------------------------------------------------- NEXT-2 producers
+def f64_to_bf16(d: float) -> int:
+    """binary64 -> BF16 bits, round to nearest even (no double rounding)."""
+    return int(_load().oracle_f64_to_bf16(float(d)))
+
+
+def rmsnorm_bf16(x_bits: np.ndarray, gamma_bits: np.ndarray, eps: float) -> np.ndarray:
+    """y = BF16_RNE(x / sqrt(mean(x^2) + eps) * gamma), binary64 inside."""
+    x = _as_bf16_bits(x_bits)
+    g = _as_bf16_bits(gamma_bits)
+    m, k = x.shape
+    if g.shape != (k,):
+        raise OracleError("gamma must have shape [k]")
+    y = np.empty((m, k), dtype=np.uint16)
+    _load().oracle_rmsnorm_bf16(_ptr(x), m, k, _ptr(g), float(eps), _ptr(y))
+    return y
+
+
+def silu_mul_bf16(gate_up_bits: np.ndarray) -> np.ndarray:
+    """y = BF16_RNE(silu(gate) * up) for gate_up = [gate | up] (each [m, I]), binary64 inside."""
+    gu = _as_bf16_bits(gate_up_bits)
+    m, k2 = gu.shape
+    if k2 % 2:
+        raise OracleError("gate_up must have an even number of columns")
+    y = np.empty((m, k2 // 2), dtype=np.uint16)
+    _load().oracle_silu_mul_bf16(_ptr(gu), m, k2 // 2, _ptr(y))
+    return y
+
+
+def rmsnorm_quantize(x_bits, gamma_bits, eps, nthreads=None):
+    """NEXT-2 definition: per-token-group quantization (O3-O6) of the BF16 RMSNorm output."""
+    y = rmsnorm_bf16(x_bits, gamma_bits, eps)
+    return (y,) + quantize_act_per_token_group(y, nthreads)
+
+
+def silu_mul_quantize(gate_up_bits, nthreads=None):
+    """NEXT-2 definition: per-token-group quantization of the BF16 SiLU(gate) * up output."""
+    y = silu_mul_bf16(gate_up_bits)
+    return (y,) + quantize_act_per_token_group(y, nthreads)

@@ -308,3 +308,64 @@ int oracle_gemm_rows(const uint8_t* a, int64_t ld_a, const float* sa, int64_t ld
     parallel_for(gemm_range, &c, nrows, nthreads);
     return ORACLE_OK;
 }
+
+/* ================================================================== NEXT-2: producers
+ * the activation quantizer's producers on the Qwen3 rollout forward,
+ * RMSNorm (input of qkv and gate_up) and SiLU(gate) * up (input of down_proj).  The
+ * unfused pipeline materialises the producer's output in BF16 and then quantizes it
+ * (PAPER.md:65,73), so the oracle's definition is:  y = BF16_RNE(f(x)) with f evaluated in
+ * binary64, then O3-O6 per-token-group quantization of y.
+ *   RMSNorm:   f(x)_j = x_j / sqrt(mean_i(x_i^2) + eps) * gamma_j
+ *   SiLU-mul:  f(g, u) = g / (1 + exp(-g)) * u
+ */
+
+/* binary64 -> BF16 bits, round to nearest even (direct: no double rounding through fp32). */
+uint16_t oracle_f64_to_bf16(double d) {
+    if (isnan(d)) return 0x7FC0;
+    uint16_t sign = signbit(d) ? 0x8000 : 0;
+    double a = fabs(d);
+    if (a == 0.0) return sign;
+    if (isinf(a)) return sign | 0x7F80;
+    int e;
+    frexp(a, &e); /* a = f * 2^e, f in [0.5, 1) */
+    /* quantum of the result: 2^(e-8) for normals (8 significant bits), 2^-133 below 2^-126 */
+    int qexp = e - 8;
+    if (qexp < -133) qexp = -133;
+    double r = nearbyint(ldexp(a, -qexp)); /* RNE, exact */
+    double v = ldexp(r, qexp);
+    if (v > 3.3895313892515355e38) return sign | 0x7F80; /* overflow to inf */
+    float f = (float)v; /* exact: <= 8 significant bits */
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return sign | (uint16_t)((u >> 16) & 0x7FFF);
+}
+
+void oracle_rmsnorm_bf16(const uint16_t* x, int64_t m, int64_t k, const uint16_t* gamma, double eps,
+                         uint16_t* y) {
+    for (int64_t r = 0; r < m; ++r) {
+        double ss = 0.0;
+        for (int64_t j = 0; j < k; ++j) {
+            double v = (double)oracle_bf16_to_float(x[r * k + j]);
+            ss += v * v;
+        }
+        double inv = 1.0 / sqrt(ss / (double)k + eps);
+        for (int64_t j = 0; j < k; ++j) {
+            double v = (double)oracle_bf16_to_float(x[r * k + j]);
+            double gj = (double)oracle_bf16_to_float(gamma[j]);
+            y[r * k + j] = oracle_f64_to_bf16(v * inv * gj);
+        }
+    }
+}
+
+void oracle_silu_mul_bf16(const uint16_t* gate_up, int64_t m, int64_t inter, uint16_t* y) {
+    for (int64_t r = 0; r < m; ++r) {
+        const uint16_t* g = gate_up + r * 2 * inter;
+        const uint16_t* u = g + inter;
+        for (int64_t j = 0; j < inter; ++j) {
+            double gv = (double)oracle_bf16_to_float(g[j]);
+            double uv = (double)oracle_bf16_to_float(u[j]);
+            double silu = gv / (1.0 + exp(-gv));
+            y[r * inter + j] = oracle_f64_to_bf16(silu * uv);
+        }
+    }
+}
