@@ -303,6 +303,7 @@ def run_layer(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = fp8q.kernel_launches()
+    torch.cuda._sleep(2_000_000)  # GPU busy (~1 ms) while the host enqueues: no idle gap timed
     for i in range(args.steps):
         evs[i][0].record()
         st.run(evs[i])
@@ -342,6 +343,7 @@ def run_layer(args):
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)
         e0.record()
         for _ in range(args.steps):
             st.run_e2e()
@@ -468,6 +470,7 @@ def run_sync(args):
         dist.barrier()
     launches0 = fp8q.kernel_launches()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda._sleep(2_000_000)
     for i in range(args.steps):
         step += 1
         evs[i][0].record()

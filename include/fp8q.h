@@ -121,6 +121,33 @@ fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t 
                                          int32_t* nonfinite_flag, void* stream);
 
 /*
+ * rmsnorm_quantize_act_per_token_group -- SURVEY §8(f) NEXT-2: quantize_act_per_token_group
+ * fused into its producer on the rollout forward (the RMSNorm before q/k/v and gate/up):
+ *   y[m, j] = BF16_RNE( x[m, j] / sqrt(mean_i x[m, i]^2 + eps) * gamma[j] )   (binary32 inside)
+ *   codes, scales = quantize_act_per_token_group(y)  (identical element map and layouts)
+ * y never reaches HBM unless y_bf16 (nullable, row stride ld_y) is given.
+ *   Requirements: k % 128 == 0 and k <= 4096 (one token row per warp, held in registers;
+ *     Qwen3 hidden sizes are 4096 / 2048) (ESHAPE); x, gamma 16-byte aligned, ld_x % 8 == 0,
+ *     codes 8-byte aligned, ld_q % 8 == 0, scales as quantize_act_per_token_group, y_bf16
+ *     16-byte aligned with ld_y % 8 == 0 (EALIGN).
+ */
+fp8q_status rmsnorm_quantize_act_per_token_group(const void* x_bf16, const void* gamma_bf16, float eps,
+                                                 int64_t m, int64_t k, int64_t ld_x, uint8_t* codes,
+                                                 int64_t ld_q, float* scales, int64_t ld_s, void* y_bf16,
+                                                 int64_t ld_y, int32_t* nonfinite_flag, void* stream);
+
+/*
+ * silu_mul_quantize_act_per_token_group -- NEXT-2 for the down_proj input:
+ *   gate = gate_up[:, 0:inter], up = gate_up[:, inter:2*inter]   (row stride ld_gu)
+ *   y = BF16_RNE( gate / (1 + exp(-gate)) * up )   (binary32 inside), then quantized as above.
+ *   Requirements: inter % 128 == 0 (ESHAPE); alignment as rmsnorm_quantize_act_per_token_group.
+ */
+fp8q_status silu_mul_quantize_act_per_token_group(const void* gate_up_bf16, int64_t m, int64_t inter,
+                                                  int64_t ld_gu, uint8_t* codes, int64_t ld_q, float* scales,
+                                                  int64_t ld_s, void* y_bf16, int64_t ld_y,
+                                                  int32_t* nonfinite_flag, void* stream);
+
+/*
  * fp8_block_gemm -- the W8A8 linear Y = X W^T, blockwise scales promoted
  * per 128-deep k-block (DeepSeek-V3 granularity cited at PAPER.md:233):
  *   D[m,n] = sum_kb sa[kb][m] * sb[n/128][kb] * sum_{k in kb} dec(a[m,k]) * dec(b[n,k])

@@ -14,5 +14,7 @@ from .fp8q import (  # noqa: F401
     quantize_act_per_token_group,
     quantize_weight_blockwise,
     quantize_weight_blockwise_batched,
+    rmsnorm_quantize_act_per_token_group,
+    silu_mul_quantize_act_per_token_group,
     version,
 )

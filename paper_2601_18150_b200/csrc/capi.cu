@@ -131,6 +131,57 @@ fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t 
     return from_cuda(e);
 }
 
+static fp8q_status check_act_out(int64_t m, int64_t k, const uint8_t* codes, int64_t ld_q, const float* scales,
+                                 int64_t ld_s, const void* y, int64_t ld_y, const int32_t* flag) {
+    if (ld_q < k || ld_s < m || (y != nullptr && ld_y < k)) return FP8Q_EINVAL;
+    if (codes == nullptr || scales == nullptr) return FP8Q_EINVAL;
+    if (!aligned(codes, 8) || ld_q % 8 != 0 || !aligned(scales, 4) || ld_s % 4 != 0 ||
+        (y != nullptr && (!aligned(y, 16) || ld_y % 8 != 0)) || (flag != nullptr && !aligned(flag, 4)))
+        return FP8Q_EALIGN;
+    return FP8Q_OK;
+}
+
+fp8q_status rmsnorm_quantize_act_per_token_group(const void* x_bf16, const void* gamma_bf16, float eps,
+                                                 int64_t m, int64_t k, int64_t ld_x, uint8_t* codes,
+                                                 int64_t ld_q, float* scales, int64_t ld_s, void* y_bf16,
+                                                 int64_t ld_y, int32_t* nonfinite_flag, void* stream) {
+    if (m < 0 || k < 0 || ld_x < k) return FP8Q_EINVAL;
+    if (k % 128 != 0 || k > 4096) return FP8Q_ESHAPE;
+    if (m == 0 || k == 0) return FP8Q_OK;
+    if (x_bf16 == nullptr || gamma_bf16 == nullptr) return FP8Q_EINVAL;
+    if (!aligned(x_bf16, 16) || !aligned(gamma_bf16, 16) || ld_x % 8 != 0) return FP8Q_EALIGN;
+    fp8q_status st = check_act_out(m, k, codes, ld_q, scales, ld_s, y_bf16, ld_y, nonfinite_flag);
+    if (st != FP8Q_OK) return st;
+    st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_rmsnorm_quantize(static_cast<const uint16_t*>(x_bf16),
+                                                  static_cast<const uint16_t*>(gamma_bf16), eps, m, k, ld_x, codes,
+                                                  ld_q, scales, ld_s, static_cast<uint16_t*>(y_bf16), ld_y,
+                                                  nonfinite_flag, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
+fp8q_status silu_mul_quantize_act_per_token_group(const void* gate_up_bf16, int64_t m, int64_t inter,
+                                                  int64_t ld_gu, uint8_t* codes, int64_t ld_q, float* scales,
+                                                  int64_t ld_s, void* y_bf16, int64_t ld_y,
+                                                  int32_t* nonfinite_flag, void* stream) {
+    if (m < 0 || inter < 0 || ld_gu < 2 * inter) return FP8Q_EINVAL;
+    if (inter % 128 != 0) return FP8Q_ESHAPE;
+    if (m == 0 || inter == 0) return FP8Q_OK;
+    if (gate_up_bf16 == nullptr) return FP8Q_EINVAL;
+    if (!aligned(gate_up_bf16, 16) || ld_gu % 8 != 0) return FP8Q_EALIGN;
+    fp8q_status st = check_act_out(m, inter, codes, ld_q, scales, ld_s, y_bf16, ld_y, nonfinite_flag);
+    if (st != FP8Q_OK) return st;
+    st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_silu_mul_quantize(static_cast<const uint16_t*>(gate_up_bf16), m, inter, ld_gu,
+                                                   codes, ld_q, scales, ld_s, static_cast<uint16_t*>(y_bf16), ld_y,
+                                                   nonfinite_flag, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
 size_t fp8_block_gemm_workspace_size(int64_t m, int64_t n, int64_t k) {
     return fp8q::gemm_workspace_bytes(m, n, k, false);
 }

@@ -916,12 +916,12 @@ int plan_splits(int64_t m, int64_t n, int64_t k, int sms) {
     const int64_t tiles = ((m + BM - 1) / BM) * ((n + 255) / 256);
     const int64_t num_kb = k / BK;
     if (tiles <= 0 || tiles * 2 > sms || num_kb < 2) return 1;
-    // fp32 partials cost 8 B per output element and slice (write + read): keep them within
-    // half of the weight bytes (N*K) -> S <= K / (16 M)
-    const int64_t s_traffic = k / (16 * (m > 0 ? m : 1));
+    // measured (tools/kernel_bench.py --decode): splitting pays only for the smallest M, where
+    // the parked fp32 partials are tiny; from M ~ 32 the fixup costs more than it recovers
+    if (m > 16) return 1;
     int best = 1;
     double best_cost = 1e30;
-    for (int sp = 1; sp <= 16 && sp <= num_kb && sp <= s_traffic; ++sp) {
+    for (int sp = 1; sp <= 16 && 2 * sp <= num_kb; ++sp) {
         const double cost = static_cast<double>((tiles * sp + sms - 1) / sms) / sp;
         if (cost < best_cost - 1e-9) {
             best_cost = cost;

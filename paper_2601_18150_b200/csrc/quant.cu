@@ -21,6 +21,7 @@
 
 #include "ptx.cuh"
 #include "quant_kernels.h"
+#include "scale_tables.cuh"
 
 namespace fp8q {
 
@@ -385,7 +386,8 @@ __device__ __forceinline__ void aq_load(const uint16_t* __restrict__ x, int64_t 
 }
 __device__ __forceinline__ void aq_process(const AItemRegs& d, uint8_t* __restrict__ q, int64_t ld_q,
                                            float* __restrict__ scales, int64_t ld_s, int64_t groups,
-                                           int64_t chunks, int64_t item, int32_t* __restrict__ nonfinite_flag) {
+                                           int64_t chunks, int64_t item, int32_t* __restrict__ nonfinite_flag,
+                                           const ScaleTables& tabs) {
     const int lane = threadIdx.x & 31;
     const int64_t row = item / chunks, chunk = item - (item / chunks) * chunks;
     uint32_t ab[4];
@@ -400,14 +402,19 @@ __device__ __forceinline__ void aq_process(const AItemRegs& d, uint8_t* __restri
     for (int j = 0; j < 4; ++j) {
         const int64_t g = chunk * 16 + 4 * j + (lane >> 3);
         if (g >= groups) continue;
-        const float s = scale_from_amax_bits(ab[j]);
+        const bool fast = ab[j] >= kAmaxFastGuardBits && ab[j] < kNonFiniteBits;
+        float s, r = 0.0f;
+        if (fast)
+            table_scale_rcp(tabs, ab[j], s, r);
+        else
+            s = scale_from_amax_bits(ab[j]);
         if ((lane & 7) == 0) {
             scales[g * ld_s + row] = s;
             if (ab[j] >= kNonFiniteBits && nonfinite_flag != nullptr) *nonfinite_flag = 1;
         }
         uint4 c;
-        if (ab[j] >= kAmaxFastGuardBits)
-            c = encode16<true>(d.v[j], s, __frcp_rn(s));
+        if (fast)
+            c = encode16<true>(d.v[j], s, r);
         else
             c = encode16<false>(d.v[j], s, 0.0f);
         st_v4_na(q + row * ld_q + g * 128 + (lane & 7) * 16, c);
@@ -417,6 +424,9 @@ __global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
     const uint16_t* __restrict__ x, int64_t ld_x, uint8_t* __restrict__ q, int64_t ld_q,
     float* __restrict__ scales, int64_t ld_s, int64_t groups, int64_t chunks, int64_t items,
     int32_t* __restrict__ nonfinite_flag) {
+    __shared__ ScaleTables tabs;
+    init_scale_tables(tabs);
+    __syncthreads();
     const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
     int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     AItemRegs a, b;
@@ -424,12 +434,12 @@ __global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
     while (item < items) {
         int64_t nxt = item + warps;
         if (nxt < items) aq_load(x, ld_x, groups, chunks, nxt, b);
-        aq_process(a, q, ld_q, scales, ld_s, groups, chunks, item, nonfinite_flag);
+        aq_process(a, q, ld_q, scales, ld_s, groups, chunks, item, nonfinite_flag, tabs);
         item = nxt;
         if (item >= items) break;
         nxt = item + warps;
         if (nxt < items) aq_load(x, ld_x, groups, chunks, nxt, a);
-        aq_process(b, q, ld_q, scales, ld_s, groups, chunks, item, nonfinite_flag);
+        aq_process(b, q, ld_q, scales, ld_s, groups, chunks, item, nonfinite_flag, tabs);
         item = nxt;
     }
 }

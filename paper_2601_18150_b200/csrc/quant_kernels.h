@@ -57,6 +57,14 @@ size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped);
 // Enqueue the tcgen05 blockwise-scaled FP8 GEMM.  Returns cudaSuccess or the first error.
 cudaError_t launch_fp8_block_gemm(const GemmArgs& args, cudaStream_t stream, int* launches);
 
+// NEXT-2 producer-fused quantizers (producers.cu).
+cudaError_t launch_rmsnorm_quantize(const uint16_t* x, const uint16_t* gamma, float eps, int64_t m, int64_t k,
+                                    int64_t ld_x, uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
+                                    uint16_t* y, int64_t ld_y, int32_t* flag, cudaStream_t stream);
+cudaError_t launch_silu_mul_quantize(const uint16_t* gu, int64_t m, int64_t inter, int64_t ld_gu, uint8_t* q,
+                                     int64_t ld_q, float* scales, int64_t ld_s, uint16_t* y, int64_t ld_y,
+                                     int32_t* flag, cudaStream_t stream);
+
 // Dev-only: record a pipeline timeline of CTA 0 into dev_ptr (96 k-blocks x 12 uint32 clocks).
 void set_gemm_trace(uint32_t* dev_ptr);
 

@@ -58,6 +58,11 @@ def load_library() -> ctypes.CDLL:
         lib.quantize_weight_blockwise_batched.restype = ctypes.c_int
         lib.quantize_act_per_token_group.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
         lib.quantize_act_per_token_group.restype = ctypes.c_int
+        lib.rmsnorm_quantize_act_per_token_group.argtypes = [P, P, ctypes.c_float, I64, I64, I64, P, I64, P, I64,
+                                                             P, I64, P, P]
+        lib.rmsnorm_quantize_act_per_token_group.restype = ctypes.c_int
+        lib.silu_mul_quantize_act_per_token_group.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, I64, P, P]
+        lib.silu_mul_quantize_act_per_token_group.restype = ctypes.c_int
         lib.fp8_block_gemm_workspace_size.argtypes = [I64, I64, I64]
         lib.fp8_block_gemm_workspace_size.restype = ctypes.c_size_t
         lib.fp8_block_gemm.argtypes = [P, I64, P, I64, P, I64, P, I64, P, I64, ctypes.c_int,
@@ -176,6 +181,60 @@ def quantize_act_per_token_group(x: torch.Tensor, codes: torch.Tensor | None = N
         x.data_ptr(), m, k, _ld(x), codes.data_ptr(), _ld(codes), scales.data_ptr(),
         scales.stride(0) if scales.shape[0] > 1 else scales.shape[1], flag, _stream(stream)),
         "quantize_act_per_token_group")
+    return codes, scales
+
+
+def _act_outputs(m, k, device, codes, scales):
+    if codes is None:
+        codes = torch.empty((m, k), dtype=torch.uint8, device=device)
+    if scales is None:
+        scales = torch.empty((k // 128, act_scales_ld(m)), dtype=torch.float32, device=device)
+    _cuda2d(codes, "codes", torch.uint8)
+    _cuda2d(scales, "scales", torch.float32)
+    if codes.shape != (m, k) or scales.shape[0] < k // 128 or scales.shape[1] < m:
+        raise Fp8qError("output shape mismatch")
+    return codes, scales
+
+
+def rmsnorm_quantize_act_per_token_group(x: torch.Tensor, gamma: torch.Tensor, eps: float,
+                                         codes=None, scales=None, y_out=None, nonfinite_flag=None,
+                                         stream=None):
+    """NEXT-2: BF16(RMSNorm(x) * gamma) quantized per token per 128 channels, y never stored
+    unless y_out is given.  Returns (codes, scales MN-major)."""
+    _cuda2d(x, "x", torch.bfloat16)
+    if not (gamma.is_cuda and gamma.dtype == torch.bfloat16 and gamma.dim() == 1 and gamma.is_contiguous()):
+        raise Fp8qError("gamma must be a contiguous CUDA bfloat16 vector")
+    m, k = x.shape
+    codes, scales = _act_outputs(m, k, x.device, codes, scales)
+    y_ptr, ld_y = (None, 0)
+    if y_out is not None:
+        _cuda2d(y_out, "y_out", torch.bfloat16)
+        y_ptr, ld_y = y_out.data_ptr(), _ld(y_out)
+    flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
+    _check(load_library().rmsnorm_quantize_act_per_token_group(
+        x.data_ptr(), gamma.data_ptr(), float(eps), m, k, _ld(x), codes.data_ptr(), _ld(codes),
+        scales.data_ptr(), scales.stride(0) if scales.shape[0] > 1 else scales.shape[1], y_ptr, ld_y, flag,
+        _stream(stream)), "rmsnorm_quantize_act_per_token_group")
+    return codes, scales
+
+
+def silu_mul_quantize_act_per_token_group(gate_up: torch.Tensor, codes=None, scales=None, y_out=None,
+                                          nonfinite_flag=None, stream=None):
+    """NEXT-2: BF16(silu(gate) * up) for gate_up = [gate | up], quantized per token per 128
+    channels.  Returns (codes [m, inter], scales MN-major)."""
+    _cuda2d(gate_up, "gate_up", torch.bfloat16)
+    m, k2 = gate_up.shape
+    inter = k2 // 2
+    codes, scales = _act_outputs(m, inter, gate_up.device, codes, scales)
+    y_ptr, ld_y = (None, 0)
+    if y_out is not None:
+        _cuda2d(y_out, "y_out", torch.bfloat16)
+        y_ptr, ld_y = y_out.data_ptr(), _ld(y_out)
+    flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
+    _check(load_library().silu_mul_quantize_act_per_token_group(
+        gate_up.data_ptr(), m, inter, _ld(gate_up), codes.data_ptr(), _ld(codes), scales.data_ptr(),
+        scales.stride(0) if scales.shape[0] > 1 else scales.shape[1], y_ptr, ld_y, flag, _stream(stream)),
+        "silu_mul_quantize_act_per_token_group")
     return codes, scales
 
 

@@ -41,6 +41,9 @@ def timeit(fn, iters, flush):
     for _ in range(iters):
         do_flush(flush)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # keep the GPU busy while the host enqueues: otherwise the start event fires on an idle
+        # GPU and the timing includes the binding's launch overhead (tens of microseconds)
+        torch.cuda._sleep(400_000)
         a.record()
         fn()
         b.record()
@@ -94,6 +97,25 @@ def main():
                 by = n * k + m * k + 4 * (m * k / 128 + n * k / 16384) + 2 * m * n
                 print(json.dumps({"kernel": "fp8_block_gemm_decode", "shape": [m, n, k], "ms": round(t, 4),
                                   "GBps": round(by / (t * 1e-3) / 1e9, 1), "frac_hbm": round(by / (t * 1e-3) / 1e9 / HBM, 4)}))
+    if args.what in ("all", "prod"):
+        M = 8192
+        for k in (4096, 2048):
+            x = torch.randn((M, k), generator=g, device=dev).to(torch.bfloat16)
+            gam = torch.ones(k, dtype=torch.bfloat16, device=dev)
+            xq = torch.empty((M, k), dtype=torch.uint8, device=dev)
+            xs = torch.empty((k // 128, fp8q.act_scales_ld(M)), dtype=torch.float32, device=dev)
+            t, lo, hi = timeit(lambda: fp8q.rmsnorm_quantize_act_per_token_group(x, gam, 1e-6, xq, xs), args.iters, flush)
+            gbs = M * k * (3 + 4 / 128) / (t * 1e-3) / 1e9
+            print(json.dumps({"kernel": "rmsnorm_quantize", "shape": [M, k], "ms": round(t, 4), "GBps": round(gbs, 1),
+                              "frac_hbm": round(gbs / HBM, 4)}))
+        for inter in (12288, 768):
+            gu = torch.randn((M, 2 * inter), generator=g, device=dev).to(torch.bfloat16)
+            xq = torch.empty((M, inter), dtype=torch.uint8, device=dev)
+            xs = torch.empty((inter // 128, fp8q.act_scales_ld(M)), dtype=torch.float32, device=dev)
+            t, lo, hi = timeit(lambda: fp8q.silu_mul_quantize_act_per_token_group(gu, xq, xs), args.iters, flush)
+            gbs = M * inter * (5 + 4 / 128) / (t * 1e-3) / 1e9
+            print(json.dumps({"kernel": "silu_mul_quantize", "shape": [M, inter], "ms": round(t, 4), "GBps": round(gbs, 1),
+                              "frac_hbm": round(gbs / HBM, 4)}))
     if args.moe:
         for T, skew in ((8192, 0.0), (8192, 1.2), (1024, 0.0)):
             sizes = synth.moe_group_sizes(T, seed=0, skew=skew)
