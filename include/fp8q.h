@@ -159,10 +159,14 @@ fp8q_status silu_mul_quantize_act_per_token_group(const void* gate_up_bf16, int6
  *   workspace / workspace_bytes: optional (NULL / 0 allowed).  With at least
  *           fp8_block_gemm_workspace_size(m, n, k) bytes (256-byte aligned, ZERO-FILLED before
  *           its first use; every launch leaves it zeroed again), small-M problems (decode,
- *           M < 256) split the K loop over more CTAs: slices park fp32 partials in the
+ *           M <= 128) split the K loop over more CTAs: slices park fp32 partials in the
  *           workspace and the last slice of each tile sums them in slice order
  *           (deterministic).  Without it the same problem runs unsplit (slower, equally
  *           correct).  A workspace must not be shared by concurrently running GEMMs.
+ *   Kernels: 1 <= m <= 128 with 16-byte-aligned a_scales and ld_sa % 4 == 0 runs the swap-AB
+ *     decode kernel (weight rows in the MMA M dimension, tokens in N); otherwise the
+ *     128 x 256 / 256 x 256 (CTA pair) tile kernel.  Both compute the same per-k-block
+ *     promotion in the same k order.
  *   Requirements: k % 128 == 0, n % 8 == 0 (ESHAPE); a, b 16-byte aligned with ld_a % 16 ==
  *     0 and ld_b % 16 == 0 (TMA); d 16-byte aligned with ld_d * sizeof(out) % 16 == 0;
  *     a_scales/b_scales 4-byte aligned (EALIGN).  m == 0 or n == 0 is a no-op; k == 0 writes 0.

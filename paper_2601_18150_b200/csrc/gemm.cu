@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <type_traits>
@@ -1054,13 +1055,16 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
 }  // namespace
 
 void set_gemm_trace(uint32_t* dev_ptr) { g_trace = dev_ptr; }
+uint32_t* get_gemm_trace() { return g_trace; }
 
 size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped) {
     if (grouped || m <= 0 || n <= 0 || k <= 0) return 0;
     int sms = 0;
     if (device_info(sms) != cudaSuccess) sms = 148;
     if (m >= 2 * BM) return 0;  // the CTA-pair kernel does not split K
-    return split_ws_bytes(m, n, plan_splits(m, n, k, sms));
+    size_t need = split_ws_bytes(m, n, plan_splits(m, n, k, sms));
+    if (m <= kSkinnyMaxM) need = std::max(need, skinny_workspace_bytes(m, n, k));
+    return need;
 }
 
 cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* launches) {
@@ -1068,6 +1072,11 @@ cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* l
     if (a.m == 0 || a.n == 0 || a.groups == 0) return cudaSuccess;
     auto encode = tensor_map_encoder();
     if (encode == nullptr) return cudaErrorNotSupported;
+    if (skinny_gemm_applies(a)) {
+        const cudaError_t es = launch_fp8_gemm_skinny(a, reinterpret_cast<void*>(encode), stream);
+        if (es == cudaSuccess) *launches = 1;
+        return es;
+    }
     int sms = 0;
     cudaError_t e = device_info(sms);
     if (e != cudaSuccess) return e;

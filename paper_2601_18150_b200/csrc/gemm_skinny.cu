@@ -1,0 +1,585 @@
+// gemm_skinny.cu -- blockwise-scaled FP8 GEMM for decode-sized M (M <= 128).
+//
+// Same result as gemm.cu:
+//     D[m,n] = sum_kb (sa[kb][m] * sb[n/128][kb]) * P_kb[m,n]
+// but with the operands swapped so the tiny token count sits in the MMA's N dimension:
+//     D^T tile [128 weight rows x MT tokens] = W_tile[128 x K] * X[MT x K]^T
+// At M <= 128 the problem is a weight stream (arithmetic intensity <= 2M flop per weight byte,
+// below the FP8/HBM ridge), so what matters is keeping every SM's TMA queue full of weight
+// tiles.  The work is the sequence of (128-row weight tile = one scale n-block, k-block)
+// pairs, T = tiles * k/128 of them, cut into G equal contiguous ranges, one per CTA of a
+// persistent grid (stream-K): every SM streams the same number of weight bytes (+-1 k-block)
+// whatever the tile count, and the ring holds 6-11 k-blocks of weights in flight per SM.  A
+// range is walked as segments (its part of each tile); a tile covered by several CTAs is
+// finished by a deterministic fixup (below).
+//
+// CTA = 12 warps (3 warpgroups):
+//   warp 0       TMA producer: per k-block W 128x128 B, X MTx128 B (rows >= m zero-filled by
+//                the tensor map) and the k-block's MT activation scales (one TMA row of the
+//                MN-major scale matrix) into a 6-11-stage ring (128-byte swizzle).
+//   warp 1       TMEM owner + MMA issuer: 4 x tcgen05.mma.kind::f8f6f4 (M=128, N=MT, K=32)
+//                per k-block into TMEM buffer it % NBUF (fresh accumulation per k-block).
+//   warps 2, 3   idle (they only give their registers to the promotion warps).
+//   warps 4..11  promotion: warp w reads TMEM lanes 32*(w%4).. (its 32 weight rows) and half
+//                of the MT token columns; acc[j] += P_kb[j] * (sa[kb][j] * sb[nb][kb]) (the
+//                same fp32 operations, in the same k order, as gemm.cu), scales from the
+//                stage (no dependent global load in the k-loop).  A segment that covers a
+//                whole tile is stored at once (BF16 = RNE of the fp32 value).  A partial
+//                segment (only the first and the last of a CTA's range can be partial) parks
+//                its fp32 partial in the workspace without waiting; after its range the CTA
+//                fences once and, per parked tile, bumps the tile's counter: the last CTA of
+//                the tile to arrive sums every CTA's partial in CTA order (deterministic: the
+//                order never depends on which CTA arrives last) and stores the tile.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "ptx.cuh"
+#include "quant_kernels.h"
+
+namespace fp8q {
+namespace {
+
+constexpr int SK_BN = 128;  // weight rows per tile (MMA M) = one scale n-block
+constexpr int SK_BK = 128;
+constexpr int SK_THREADS = 384;   // warpgroup 0: TMA, MMA, 2 idle; warpgroups 1-2: promotion
+constexpr int SK_EPI_WARP0 = 4;
+// setmaxnreg: warpgroup 0 drops to 72 registers so the promotion warpgroups can take 216
+// (the CTA's pool is fixed at launch: 384 x 168 = 128 x 72 + 256 x 216).
+constexpr int SK_REGS_CTRL = 72;
+constexpr int SK_REGS_EPI = 216;
+static_assert(128 * (168 - SK_REGS_CTRL) >= 256 * (SK_REGS_EPI - 168), "register pool overdrawn");
+constexpr int SK_EPI_WARPS = 8;
+constexpr int SK_SMEM_BUDGET = 200 * 1024;
+constexpr size_t SK_COUNTER_BYTES = 4096;  // one int32 per tile: up to 1024 tiles (N <= 131072)
+constexpr int SK_MAX_SPLITS = 16;
+
+constexpr int pow2_at_least(int v, int lo) {
+    int p = lo;
+    while (p < v) p *= 2;
+    return p;
+}
+
+template <int MT>
+struct SkCfg {
+    static constexpr int W_TILE = SK_BN * SK_BK;   // 16 KB
+    static constexpr int X_TILE = MT * SK_BK;      // MT x 128 B (a multiple of 1024 B: SW128 atoms)
+    static constexpr int SA_BYTES = MT * 4;                          // TMA box bytes
+    static constexpr int SA_SLOT = SA_BYTES < 128 ? 128 : SA_BYTES;  // TMA smem dst: 128-B aligned
+    static constexpr int STAGE_BYTES = W_TILE + X_TILE;
+    static constexpr int STAGES_RAW = SK_SMEM_BUDGET / (STAGE_BYTES + SA_SLOT);
+    static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
+    static constexpr int NBUF_RAW = 512 / MT;
+    static constexpr int NBUF = NBUF_RAW > 8 ? 8 : NBUF_RAW;  // TMEM partial buffers
+    static constexpr int TMEM_COLS = pow2_at_least(NBUF * MT, 32);
+    static constexpr int COLS = MT / 2;  // token columns per promotion thread
+    static constexpr uint32_t IDESC = idesc_e4m3_f32(SK_BN, MT);
+    static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * (STAGE_BYTES + SA_SLOT) + 512;
+    static_assert(MT % 16 == 0 && MT >= 16 && MT <= 128, "MMA N for M=128 must be a multiple of 16");
+    static_assert(X_TILE % 1024 == 0, "X tile must be whole 128-byte-swizzle atoms");
+};
+
+struct SkParams {
+    const float* sb;
+    int64_t ld_sb;
+    void* d;
+    int64_t ld_d;
+    int out_f32;
+    int m, n, num_kb, tiles;
+    int streamk;        // 1: ranges [c*T/G, (c+1)*T/G) per CTA; 0: whole tiles, strided
+    int64_t total;      // T = tiles * num_kb
+    float* ws;          // stream-K partials: two [MT][128] fp32 slots per CTA
+    int32_t* counters;  // [tiles], left zeroed
+    uint32_t* trace;    // dev timeline of CTA 0 (tools/gemm_trace.py), normally null
+};
+
+// dev timeline (CTA 0, SM clock): per k-block 0 producer issue, 1 MMA sees the stage full,
+// 2 promotion sees the partial, 3 promotion done;
+// row 0 also 4 entry, 5 after setup, 6 exit
+__device__ __forceinline__ void sk_trace(const SkParams& p, uint32_t it, int ev) {
+    if (p.trace != nullptr && blockIdx.x == 0 && it < 96) p.trace[it * 12 + ev] = static_cast<uint32_t>(clock64());
+}
+// every CTA's entry / exit on the global timer (ns): trace[1152 + 2 b + {0, 1}]
+__device__ __forceinline__ void sk_trace_cta(const SkParams& p, int which) {
+    if (p.trace != nullptr && blockIdx.x < 256) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        p.trace[1152 + 2 * blockIdx.x + which] = static_cast<uint32_t>(t);
+    }
+}
+
+// Walks this CTA's segments: (tile, kb0, kb1) = k-blocks [kb0, kb1) of weight tile `tile`.
+struct SegIter {
+    int64_t x, end;  // stream-K: position in [0, T) and this CTA's range end
+    int t;           // tiled: next tile
+    __device__ __forceinline__ void init(const SkParams& p) {
+        if (p.streamk) {
+            x = static_cast<int64_t>(blockIdx.x) * p.total / gridDim.x;
+            end = static_cast<int64_t>(blockIdx.x + 1) * p.total / gridDim.x;
+        }
+        t = blockIdx.x;
+    }
+    __device__ __forceinline__ bool next(const SkParams& p, int& tile, int& kb0, int& kb1) {
+        if (p.streamk) {
+            if (x >= end) return false;
+            tile = static_cast<int>(x / p.num_kb);
+            const int64_t t0 = int64_t(tile) * p.num_kb;
+            kb0 = static_cast<int>(x - t0);
+            kb1 = static_cast<int>(end - t0 < p.num_kb ? end - t0 : p.num_kb);
+            x = t0 + kb1;
+            return true;
+        }
+        if (t >= p.tiles) return false;
+        tile = t;
+        kb0 = 0;
+        kb1 = p.num_kb;
+        t += gridDim.x;
+        return true;
+    }
+};
+// The CTA whose range holds k-block position x: the largest c with floor(c T / G) <= x.
+__device__ __forceinline__ int sk_cta_of(const SkParams& p, int64_t x) {
+    return static_cast<int>(((x + 1) * gridDim.x - 1) / p.total);
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[N]);
+template <>
+__device__ __forceinline__ void tmem_ld_cols<8>(uint32_t taddr, float (&v)[8]) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "r"(taddr));
+}
+template <>
+__device__ __forceinline__ void tmem_ld_cols<16>(uint32_t taddr, float (&v)[16]) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+template <>
+__device__ __forceinline__ void tmem_ld_cols<32>(uint32_t taddr, float (&v)[32]) {
+    tmem_ld_32x32b_x32(taddr, v);
+}
+template <>
+__device__ __forceinline__ void tmem_ld_cols<64>(uint32_t taddr, float (&v)[64]) {
+    tmem_ld_32x32b_x32(taddr, *reinterpret_cast<float(*)[32]>(&v[0]));
+    tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<float(*)[32]>(&v[32]));
+}
+
+// D[j0 + j][n_row] for j < jn (a running pointer: not COLS precomputed 64-bit addresses).
+template <int COLS>
+__device__ __forceinline__ void sk_store(const SkParams& p, int64_t n_row, int j0, int jn, const float (&acc)[COLS]) {
+    if (p.out_f32) {
+        float* d = static_cast<float*>(p.d) + n_row + int64_t(j0) * p.ld_d;
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) {
+            if (j < jn) *d = acc[j];
+            d += p.ld_d;
+        }
+    } else {
+        __nv_bfloat16* d = static_cast<__nv_bfloat16*>(p.d) + n_row + int64_t(j0) * p.ld_d;
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) {
+            if (j < jn) *d = __float2bfloat16_rn(acc[j]);
+            d += p.ld_d;
+        }
+    }
+}
+
+template <int MT>
+__global__ void __launch_bounds__(SK_THREADS, 1)
+    fp8_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                           const __grid_constant__ CUtensorMap tmS, const SkParams p) {
+    using C = SkCfg<MT>;
+    constexpr int STAGES = C::STAGES;
+    constexpr int NBUF = C::NBUF;
+    constexpr int COLS = C::COLS;
+    constexpr int SA_STRIDE = C::SA_SLOT / 4;  // floats between stages' scale slots
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smW = smem;
+    uint8_t* smX = smW + STAGES * C::W_TILE;
+    float* smS = reinterpret_cast<float*>(smX + STAGES * C::X_TILE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smS + STAGES * SA_STRIDE);
+    uint64_t* empty = full + STAGES;    // the MMA consumed W and X of the stage
+    uint64_t* sempty = empty + STAGES;  // the promotion warps consumed its activation scales
+    uint64_t* tfull = sempty + STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        sk_trace(p, 0, 4);
+        sk_trace_cta(p, 0);
+    }
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+            mbar_init(&sempty[s], SK_EPI_WARPS);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], SK_EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (threadIdx.x == 0) sk_trace(p, 0, 5);
+    if (warp < SK_EPI_WARP0) regs_dec<SK_REGS_CTRL>();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ TMA producer
+            tma_prefetch_desc(&tmW);
+            tma_prefetch_desc(&tmX);
+            tma_prefetch_desc(&tmS);
+            uint32_t it = 0;
+            SegIter seg;
+            seg.init(p);
+            int tile, kb0, kb1;
+            while (seg.next(p, tile, kb0, kb1)) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const uint32_t stage = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1u;
+                    mbar_wait(&empty[stage], ph ^ 1u);
+                    mbar_wait(&sempty[stage], ph ^ 1u);
+                    sk_trace(p, it, 0);
+                    mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES + C::SA_BYTES);
+                    tma_load_2d(smW + stage * C::W_TILE, &tmW, &full[stage], kb * SK_BK, tile * SK_BN);
+                    tma_load_2d(smX + stage * C::X_TILE, &tmX, &full[stage], kb * SK_BK, 0);
+                    tma_load_2d(smS + stage * SA_STRIDE, &tmS, &full[stage], 0, kb);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ MMA issuer
+            const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+            uint32_t it = 0;
+            SegIter seg;
+            seg.init(p);
+            int tile, kb0, kb1;
+            while (seg.next(p, tile, kb0, kb1)) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const uint32_t stage = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1u;
+                    const uint32_t buf = it % NBUF;
+                    const uint32_t bph = (it / NBUF) & 1u;
+                    mbar_wait(&tempty[buf], bph ^ 1u);
+                    mbar_wait(&full[stage], ph);
+                    sk_trace(p, it, 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smW + stage * C::W_TILE);
+                    const uint32_t b0 = smem_u32(smX + stage * C::X_TILE);
+                    const uint32_t d = tmem + buf * MT;
+#pragma unroll
+                    for (int kk = 0; kk < SK_BK / 32; ++kk)
+                        mma_f8f6f4(d, smem_desc_k_sw128(a0 + kk * 32), smem_desc_k_sw128(b0 + kk * 32), C::IDESC,
+                                   kk > 0 ? 1u : 0u);
+                    mma_commit(&empty[stage]);
+                    mma_commit(&tfull[buf]);
+                }
+            }
+        }
+    } else if (warp >= SK_EPI_WARP0) {
+        // ---------------------------------------------------------------- promotion warps
+        regs_inc<SK_REGS_EPI>();
+        const int qd = warp & 3;                       // TMEM lane quarter of this warp
+        const int h = (warp - SK_EPI_WARP0) >> 2;      // token-column half
+        const int r_in = qd * 32 + lane;               // weight row within the tile
+        const int j0 = h * COLS;                       // first token column of this thread
+        const int jn = p.m - j0 < COLS ? p.m - j0 : COLS;  // live columns of this thread
+        const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+        int parked[2] = {-1, -1};  // tiles whose partial this CTA parked (slot 0 / slot 1)
+        uint32_t it = 0;
+        SegIter seg;
+        seg.init(p);
+        int tile, kb0, kb1;
+        for (int si = 0; seg.next(p, tile, kb0, kb1); ++si) {
+            const float* sbp = p.sb + int64_t(tile) * p.ld_sb;
+            float acc[COLS];
+#pragma unroll
+            for (int j = 0; j < COLS; ++j) acc[j] = 0.0f;
+            float sb_next = __ldg(sbp + kb0);
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                const float sbk = sb_next;
+                if (kb + 1 < kb1) sb_next = __ldg(sbp + kb + 1);
+                const uint32_t stage = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1u;
+                const uint32_t buf = it % NBUF;
+                const uint32_t bph = (it / NBUF) & 1u;
+                mbar_wait(&tfull[buf], bph);
+                if (threadIdx.x == SK_EPI_WARP0 * 32) sk_trace(p, it, 2);
+                mbar_wait(&full[stage], ph);  // (already complete) orders the TMA-written scales
+                tc_fence_after();
+                const float* sa_s = smS + stage * SA_STRIDE + j0;
+                // chunks of <= 16 columns keep the live registers at acc + one chunk
+                constexpr int CH = COLS < 16 ? COLS : 16;
+#pragma unroll
+                for (int c = 0; c < COLS / CH; ++c) {
+                    float v[CH];
+                    tmem_ld_cols<CH>(tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * MT + j0 + c * CH, v);
+                    tmem_wait_ld();
+                    if (c + 1 == COLS / CH) {  // the partial is in registers: hand the buffer back
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[buf]);
+                    }
+                    const float4* sa4 = reinterpret_cast<const float4*>(sa_s + c * CH);
+#pragma unroll
+                    for (int j = 0; j < CH / 4; ++j) {
+                        const float4 s4 = sa4[j];
+                        float* a = acc + c * CH + 4 * j;
+                        a[0] = __fmaf_rn(v[4 * j + 0], __fmul_rn(s4.x, sbk), a[0]);
+                        a[1] = __fmaf_rn(v[4 * j + 1], __fmul_rn(s4.y, sbk), a[1]);
+                        a[2] = __fmaf_rn(v[4 * j + 2], __fmul_rn(s4.z, sbk), a[2]);
+                        a[3] = __fmaf_rn(v[4 * j + 3], __fmul_rn(s4.w, sbk), a[3]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sempty[stage]);  // the scales were read
+                if (threadIdx.x == SK_EPI_WARP0 * 32) sk_trace(p, it, 3);
+            }
+            const int64_t n_row = int64_t(tile) * SK_BN + r_in;
+            if (kb0 > 0 || kb1 < p.num_kb) {
+                // partial tile (first or last segment of this CTA's range): park it, no wait
+                const int slot = si == 0 ? 0 : 1;
+                parked[slot] = tile;
+                float* mine = p.ws + (int64_t(2 * blockIdx.x + slot) * MT + j0) * SK_BN + r_in;
+#pragma unroll
+                for (int j = 0; j < COLS; ++j) {
+                    if (j < jn) *mine = acc[j];
+                    mine += SK_BN;
+                }
+            } else if (n_row < p.n) {
+                sk_store(p, n_row, j0, jn, acc);
+            }
+        }
+        // ---- stream-K fixup of the parked tiles (at most two per CTA): one fence, both
+        // counters bumped in one round trip, then the sums of the tiles this CTA completes
+        if (parked[0] >= 0 || parked[1] >= 0) {
+            __shared__ int sk_last[2];
+            __threadfence();
+            asm volatile("bar.sync 1, %0;" ::"n"(SK_EPI_WARPS * 32) : "memory");
+            if (threadIdx.x == SK_EPI_WARP0 * 32) {
+                int old[2] = {-1, -1};
+#pragma unroll
+                for (int slot = 0; slot < 2; ++slot)
+                    if (parked[slot] >= 0) old[slot] = atomicAdd(&p.counters[parked[slot]], 1);
+                __threadfence();
+#pragma unroll
+                for (int slot = 0; slot < 2; ++slot) {
+                    const int t = parked[slot];
+                    const int64_t t0 = int64_t(t) * p.num_kb;
+                    sk_last[slot] = t >= 0 && old[slot] == sk_cta_of(p, t0 + p.num_kb - 1) - sk_cta_of(p, t0);
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(SK_EPI_WARPS * 32) : "memory");
+#pragma unroll 1
+            for (int slot = 0; slot < 2; ++slot) {
+                if (!sk_last[slot]) continue;
+                const int t = parked[slot];
+                const int64_t t0 = int64_t(t) * p.num_kb;
+                const int c_first = sk_cta_of(p, t0);
+                const int c_last = sk_cta_of(p, t0 + p.num_kb - 1);
+                // CTA c parked tile t in slot 0 if t is the first tile of c's range, else slot 1.
+                // Unpredicated loads (columns past m hold stale values that are never stored)
+                // so each CTA's whole row segment is in flight at once.
+                float acc[COLS];
+#pragma unroll
+                for (int j = 0; j < COLS; ++j) acc[j] = 0.0f;
+#pragma unroll 1
+                for (int c = c_first; c <= c_last; ++c) {
+                    const int64_t c_start = int64_t(c) * p.total / gridDim.x;
+                    const float* src = p.ws + (int64_t(2 * c + (c_start < t0 ? 1 : 0)) * MT + j0) * SK_BN + r_in;
+                    float v[COLS];
+#pragma unroll
+                    for (int j = 0; j < COLS; ++j) v[j] = __ldcg(src + j * SK_BN);
+#pragma unroll
+                    for (int j = 0; j < COLS; ++j) acc[j] += v[j];
+                }
+                if (threadIdx.x == SK_EPI_WARP0 * 32) p.counters[t] = 0;  // reusable workspace
+                const int64_t n_row = int64_t(t) * SK_BN + r_in;
+                if (n_row < p.n) sk_store(p, n_row, j0, jn, acc);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sk_trace(p, 0, 6);
+        sk_trace_cta(p, 1);
+    }
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(*reinterpret_cast<volatile uint32_t*>(tmem_slot), C::TMEM_COLS);
+    }
+}
+
+// ------------------------------------------------------------------------------ host side
+int sk_mt(int64_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : 128; }
+
+// Stream-K grid: one CTA per SM, but at least 2 k-blocks per CTA.
+int64_t sk_grid(int64_t tiles, int64_t num_kb, int sms) {
+    const int64_t total = tiles * num_kb;
+    int64_t g = std::min<int64_t>(sms, total / 2);
+    return g < 1 ? 1 : g;
+}
+bool sk_streamk_possible(int64_t n, int64_t k, int sms) {
+    const int64_t tiles = (n + SK_BN - 1) / SK_BN;
+    return tiles * 4 <= static_cast<int64_t>(SK_COUNTER_BYTES) && sk_grid(tiles, k / SK_BK, sms) > 1;
+}
+size_t sk_ws_bytes(int64_t m, int64_t n, int64_t k, int sms) {
+    if (!sk_streamk_possible(n, k, sms)) return 0;
+    const int64_t tiles = (n + SK_BN - 1) / SK_BN;
+    return SK_COUNTER_BYTES + static_cast<size_t>(2 * sk_grid(tiles, k / SK_BK, sms)) * sk_mt(m) * SK_BN * 4;
+}
+
+struct SkDev {
+    int sms = 0;
+    bool attr_set = false;
+};
+SkDev g_sk_dev[64];
+std::mutex g_sk_mu;
+
+cudaError_t sk_device_info(int& sms) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_sk_mu);
+    SkDev& di = g_sk_dev[dev];
+    if (!di.attr_set) {
+        e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+#define SK_ATTR(MT)                                                                                      \
+    e = cudaFuncSetAttribute(fp8_gemm_skinny_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             static_cast<int>(SkCfg<MT>::SMEM_BYTES));                                 \
+    if (e != cudaSuccess) return e;
+        SK_ATTR(16)
+        SK_ATTR(32)
+        SK_ATTR(64)
+        SK_ATTR(128)
+#undef SK_ATTR
+        di.attr_set = true;
+    }
+    sms = di.sms;
+    return cudaSuccess;
+}
+
+template <int MT>
+cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encode, int sms, cudaStream_t stream) {
+    CUtensorMap tmW, tmX, tmS;
+    {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.n)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_b)};
+        cuuint32_t box[2] = {SK_BK, SK_BN};
+        cuuint32_t estr[2] = {1, 1};
+        if (encode(&tmW, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.b), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.m)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_a)};
+        cuuint32_t box[2] = {SK_BK, MT};
+        cuuint32_t estr[2] = {1, 1};
+        if (encode(&tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.a), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    {
+        // activation scales, MN-major [k/128][ld_sa]: row kb holds the m tokens' scales
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.m), static_cast<cuuint64_t>(a.k / SK_BK)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_sa * 4)};
+        cuuint32_t box[2] = {MT, 1};
+        cuuint32_t estr[2] = {1, 1};
+        if (encode(&tmS, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.sa), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    SkParams p;
+    p.sb = a.sb;
+    p.ld_sb = a.ld_sb;
+    p.d = a.d;
+    p.ld_d = a.ld_d;
+    p.out_f32 = a.out_f32 ? 1 : 0;
+    p.m = static_cast<int>(a.m);
+    p.n = static_cast<int>(a.n);
+    p.num_kb = static_cast<int>(a.k / SK_BK);
+    p.tiles = static_cast<int>((a.n + SK_BN - 1) / SK_BN);
+    p.total = int64_t(p.tiles) * p.num_kb;
+    p.streamk = 0;
+    p.ws = nullptr;
+    p.counters = nullptr;
+    p.trace = get_gemm_trace();
+    unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, sms));  // whole tiles
+    const size_t need = sk_ws_bytes(a.m, a.n, a.k, sms);
+    if (need > 0 && a.workspace != nullptr && a.workspace_bytes >= need) {
+        p.streamk = 1;
+        p.counters = static_cast<int32_t*>(a.workspace);
+        p.ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + SK_COUNTER_BYTES);
+        grid = static_cast<unsigned>(sk_grid(p.tiles, p.num_kb, sms));
+    }
+    fp8_gemm_skinny_kernel<MT><<<grid, SK_THREADS, SkCfg<MT>::SMEM_BYTES, stream>>>(tmW, tmX, tmS, p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool skinny_gemm_applies(const GemmArgs& a) {
+    static const int forced = [] {
+        const char* e = std::getenv("FP8Q_GEMM_KIND");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced != 0 && forced != 16) return false;  // dev override: 16 = skinny, others = gemm.cu kinds
+    if (a.offsets != nullptr || a.m < 1 || a.m > kSkinnyMaxM || (reinterpret_cast<uintptr_t>(a.sa) & 15u) != 0 ||
+        (a.ld_sa % 4) != 0)
+        return false;
+    // Measured (tools/kernel_bench.py --decode --graph, Qwen3-8B shapes): up to M = 32 this
+    // kernel wins everywhere; above, the 128 x 256 tile kernel wins once it has >= 64 tiles to
+    // spread (gate_up), this one where the tile kernel would leave most SMs idle (qkv, o, down).
+    return forced == 16 || a.m <= 32 || (a.n + 255) / 256 < 64;
+}
+
+size_t skinny_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+    int sms = 0;
+    if (sk_device_info(sms) != cudaSuccess) sms = 148;
+    return sk_ws_bytes(m, n, k, sms);
+}
+
+cudaError_t launch_fp8_gemm_skinny(const GemmArgs& a, void* encode_fn, cudaStream_t stream) {
+    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(encode_fn);
+    if (encode == nullptr) return cudaErrorNotSupported;
+    int sms = 0;
+    cudaError_t e = sk_device_info(sms);
+    if (e != cudaSuccess) return e;
+    switch (sk_mt(a.m)) {
+        case 16: return sk_launch<16>(a, encode, sms, stream);
+        case 32: return sk_launch<32>(a, encode, sms, stream);
+        case 64: return sk_launch<64>(a, encode, sms, stream);
+        default: return sk_launch<128>(a, encode, sms, stream);
+    }
+}
+
+}  // namespace fp8q

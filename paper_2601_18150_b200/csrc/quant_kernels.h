@@ -51,6 +51,12 @@ struct GemmArgs {
     size_t workspace_bytes;
 };
 
+// Decode-sized dense GEMMs (1 <= m <= kSkinnyMaxM) run the swap-AB kernel of gemm_skinny.cu.
+constexpr int kSkinnyMaxM = 128;
+bool skinny_gemm_applies(const GemmArgs& a);
+size_t skinny_workspace_bytes(int64_t m, int64_t n, int64_t k);
+cudaError_t launch_fp8_gemm_skinny(const GemmArgs& a, void* encode_fn, cudaStream_t stream);
+
 // Bytes of workspace with which launch_fp8_block_gemm uses split-K for this shape (0: never).
 size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped);
 
@@ -67,5 +73,6 @@ cudaError_t launch_silu_mul_quantize(const uint16_t* gu, int64_t m, int64_t inte
 
 // Dev-only: record a pipeline timeline of CTA 0 into dev_ptr (96 k-blocks x 12 uint32 clocks).
 void set_gemm_trace(uint32_t* dev_ptr);
+uint32_t* get_gemm_trace();
 
 }  // namespace fp8q

@@ -61,10 +61,12 @@ def test_gemm_wide_dynamic_range():
     assert rel_frobenius(y, oracle.gemm_rows(a, sa, b, sb)) <= 1e-5
 
 
-def test_gemm_scale_probe_bitwise():
+@pytest.mark.parametrize("m", [160, 48, 5])
+def test_gemm_scale_probe_bitwise(m):
     # every activation group / weight block is the constant +-448*2^e: codes 0x7E/0xFE,
     # scales exactly 2^e, partials exact, so D has an exact closed form.
-    m, n, k = 160, 512, 1024
+    # m <= 128 runs the swap-AB decode kernel (gemm_skinny.cu), m = 160 the tile kernel.
+    n, k = 512, 1024
     rng = np.random.default_rng(0)
     ea = rng.integers(-3, 4, size=(m, k // 128))
     ew = rng.integers(-3, 4, size=(n // 128, k // 128))
@@ -90,10 +92,12 @@ def test_gemm_bf16_is_rne_of_f32_and_deterministic():
     assert torch.equal(yf.view(torch.int32), yf2.view(torch.int32))
 
 
-@pytest.mark.parametrize("m", [1, 2, 8, 64, 192, 256])
-def test_gemm_decode_shapes(m):
-    # C3: decode-shaped GEMMs at Qwen3-8B o_proj width (K = N = 4096)
-    a, sa, b, sb = _operands(m, 4096, 4096, 20 + m)
+@pytest.mark.parametrize("m,n", [(1, 4096), (2, 4096), (8, 4096), (64, 4096), (192, 4096), (256, 4096),
+                                 (96, 16384)])
+def test_gemm_decode_shapes(m, n):
+    # C3: decode-shaped GEMMs at Qwen3-8B o_proj width (K = N = 4096); (96, 16384) takes the
+    # tile kernel (M > 32 with >= 64 column tiles), the other M <= 128 the swap-AB kernel
+    a, sa, b, sb = _operands(m, n, 4096, 20 + m)
     y = _run(a, sa, b, sb).cpu().numpy()
     assert rel_frobenius(y, oracle.gemm_rows(a, sa, b, sb)) <= TOL
 
@@ -208,12 +212,11 @@ def test_gemm_splitk_decode(m, n, k):
     ref = oracle.gemm_rows(a, sa, b, sb, np.arange(min(m, 16)))
     assert rel_frobenius(y1[:min(m, 16)].cpu().numpy(), ref) <= 1e-5
     # the same problem without a workspace runs unsplit: equal up to fp32 summation order
-    da = torch.from_numpy(a).cuda()
+    da, db, dsb = (torch.from_numpy(t).cuda() for t in (a, b, sb))  # held until the kernel ran
     dsa = act_scales_mn_from_logical(sa, fp8q.act_scales_ld(m))
     yu = torch.empty((m, n), dtype=torch.float32, device="cuda")
-    st = lib.fp8_block_gemm(da.data_ptr(), k, dsa.data_ptr(), dsa.stride(0),
-                            torch.from_numpy(b).cuda().data_ptr(), k,
-                            torch.from_numpy(sb).cuda().data_ptr(), sb.shape[1], yu.data_ptr(), n, 1,
+    st = lib.fp8_block_gemm(da.data_ptr(), k, dsa.data_ptr(), dsa.stride(0), db.data_ptr(), k,
+                            dsb.data_ptr(), sb.shape[1], yu.data_ptr(), n, 1,
                             m, n, k, None, 0, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert st == 0
@@ -228,3 +231,45 @@ def test_splitk_workspace_reused_across_shapes():
         a, sa, b, sb = _operands(m, n, k, 40 + i)
         y = _run(a, sa, b, sb).cpu().numpy()
         assert rel_frobenius(y, oracle.gemm_rows(a, sa, b, sb)) <= 1e-5, (m, n, k)
+
+
+# ------------------------------------------------------------------- decode kernel (swap-AB)
+@pytest.mark.parametrize("m,n,k", [
+    (1, 256, 128), (3, 200, 256), (16, 1000, 512), (17, 384, 1024), (33, 4096, 4096),
+    (64, 6144, 4096), (100, 1032, 1536), (127, 512, 12288), (128, 4096, 4096),
+])
+def test_skinny_decode_vs_oracle(m, n, k):
+    # 1 <= m <= 128 (dense) runs gemm_skinny.cu: tokens in the MMA N dimension (16..128 padded
+    # by the tensor map's zero fill), split-K over a persistent grid with a deterministic fixup
+    a, sa, b, sb = _operands(m, n, k, 50 + m)
+    y = _run(a, sa, b, sb)
+    rows = np.arange(m) if m <= 40 else np.unique(np.r_[0, m - 1, np.random.default_rng(m).integers(0, m, 24)])
+    ref = oracle.gemm_rows(a, sa, b, sb, rows)
+    got = y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert rel_frobenius(got, ref) <= 1e-5
+    for i in range(len(rows)):
+        assert rel_frobenius(got[i], ref[i]) <= 1e-4
+    yb = _run(a, sa, b, sb, torch.bfloat16)  # BF16 = RNE(F32), and deterministic
+    assert torch.equal(yb.view(torch.int16), y.to(torch.bfloat16).view(torch.int16))
+    assert torch.equal(_run(a, sa, b, sb).view(torch.int32), y.view(torch.int32))
+
+
+def test_skinny_matches_tile_kernel_when_scales_misaligned():
+    # activation scales at a pointer that is not 16-byte aligned cannot be TMA-loaded: the call
+    # falls back to the tile kernel (no split: no workspace), whose result must agree
+    m, n, k = 24, 768, 1024
+    a, sa, b, sb = _operands(m, n, k, 61)
+    y = _run(a, sa, b, sb)
+    ld = fp8q.act_scales_ld(m)
+    mn = act_scales_mn_from_logical(sa, ld)
+    big = torch.zeros((mn.shape[0], ld + 4), dtype=torch.float32, device="cuda")
+    big[:, 1:1 + ld] = mn
+    lib = fp8q.load_library()
+    yt = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    da, db, dsb = (torch.from_numpy(t).cuda() for t in (a, b, sb))  # held until the kernel ran
+    st = lib.fp8_block_gemm(da.data_ptr(), k, big.data_ptr() + 4, ld + 4, db.data_ptr(), k, dsb.data_ptr(),
+                            sb.shape[1], yt.data_ptr(), n, 1, m, n, k, None, 0,
+                            torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert st == 0
+    assert rel_frobenius(yt.cpu().numpy(), y.cpu().numpy()) <= 1e-6

@@ -1,0 +1,5 @@
+# bench line + launch list with DRAM bytes per launch (-> profiles/traffic.json)
+mkdir -p gpurun_out
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 120 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu=$?
+tail -2 gpurun_out/bench.json

@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Launch one kernel shape a few times (target for `ncu -k regex:... -s W -c N`).
-usage: one_gemm.py gemm M N K | wq N K | aq M K | grouped T name [skew]"""
+usage: one_gemm.py gemm M N K | wq N K | aq M K | rms M K | silu M I | grouped T name [skew]"""
 import os
 import sys
 
@@ -34,6 +34,17 @@ elif what == "aq":
     x = torch.randn((m, k), generator=g, device=dev).to(torch.bfloat16)
     for _ in range(reps):
         fp8q.quantize_act_per_token_group(x)
+elif what == "rms":
+    m, k = map(int, sys.argv[2:4])
+    x = torch.randn((m, k), generator=g, device=dev).to(torch.bfloat16)
+    gam = torch.ones(k, dtype=torch.bfloat16, device=dev)
+    for _ in range(reps):
+        fp8q.rmsnorm_quantize_act_per_token_group(x, gam, 1e-6)
+elif what == "silu":
+    m, i = map(int, sys.argv[2:4])
+    x = torch.randn((m, 2 * i), generator=g, device=dev).to(torch.bfloat16)
+    for _ in range(reps):
+        fp8q.silu_mul_quantize_act_per_token_group(x)
 elif what == "grouped":
     T = int(sys.argv[2])
     E, n, k = synth.QWEN3_30B_EXPERTS[sys.argv[3]]
