@@ -64,6 +64,10 @@ def _load():
             lib.oracle_rmsnorm_bf16.restype = None
             lib.oracle_silu_mul_bf16.argtypes = [P, I64, I64, P]
             lib.oracle_silu_mul_bf16.restype = None
+            lib.oracle_kv_amax.argtypes = [P, I64, I64, I64, P]
+            lib.oracle_kv_amax.restype = ctypes.c_int
+            lib.oracle_kv_quantize_append.argtypes = [P, I64, I64, I64, ctypes.c_float, P, P, I64]
+            lib.oracle_kv_quantize_append.restype = ctypes.c_int64
             _lib = lib
     return _lib
 
@@ -233,3 +237,44 @@ def silu_mul_quantize(gate_up_bits, nthreads=None):
     """NEXT-2 definition: per-token-group quantization of the BF16 SiLU(gate) * up output."""
     y = silu_mul_bf16(gate_up_bits)
     return (y,) + quantize_act_per_token_group(y, nthreads)
+
+
+# ---------------------------------------------------------------- NEXT-3 FP8 KV cache
+def kv_amax(x_bits: np.ndarray) -> np.float32:
+    """K1: exact max |x| over a BF16 [rows, cols] tensor.  Raises on NaN/Inf."""
+    x = _as_bf16_bits(x_bits)
+    x2 = x.reshape(x.shape[0], -1) if x.ndim > 1 else x.reshape(1, -1)
+    out = np.zeros(1, dtype=np.float32)
+    if _load().oracle_kv_amax(_ptr(x2), x2.shape[0], x2.shape[1], x2.shape[1], _ptr(out)) != 0:
+        raise OracleError("non-finite input")
+    return out[0]
+
+
+def kv_scale(amax: float) -> np.float32:
+    """K1: the layer's scalar K/V scale = O4(amax) = RN32(amax/448), 0 -> 1."""
+    return block_scale(amax)
+
+
+def kv_calibrate(batches) -> np.float32:
+    """K1 over several calibration batches (trainer side: a subset of prompts + responses):
+    the scale of the max of the per-batch amax values."""
+    return kv_scale(max(float(kv_amax(b)) for b in batches))
+
+
+def kv_quantize_append(x_bits: np.ndarray, scale: float, cache: np.ndarray, slots=None) -> int:
+    """K2-K4: codes of x's rows (scalar scale) into cache rows slots[r] (identity if None);
+    returns the saturated-element count (|RN32(x/s)| >= 464)."""
+    x = _as_bf16_bits(x_bits)
+    rows, cols = x.shape
+    if cache.dtype != np.uint8 or not cache.flags.c_contiguous or cache.shape[1] < cols:
+        raise OracleError("cache must be a C-contiguous uint8 [slots, >= cols] array")
+    sl = None
+    if slots is not None:
+        sl = np.ascontiguousarray(slots, dtype=np.int32)
+        if sl.shape != (rows,) or (rows and (sl.min() < 0 or sl.max() >= cache.shape[0])):
+            raise OracleError("slot out of range")
+    elif rows > cache.shape[0]:
+        raise OracleError("cache too small")
+    return int(_load().oracle_kv_quantize_append(_ptr(x), rows, cols, cols, float(np.float32(scale)),
+                                                 _ptr(sl) if sl is not None else None, _ptr(cache),
+                                                 cache.shape[1]))

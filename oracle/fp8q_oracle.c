@@ -369,3 +369,50 @@ void oracle_silu_mul_bf16(const uint16_t* gate_up, int64_t m, int64_t inter, uin
         }
     }
 }
+
+/* ================================================================== NEXT-3: FP8 KV cache
+ * PAPER.md §2.3.1 (lines 159-166) "dynamic QKV scale recalibration": per layer, the K (and V,
+ * Q) scale is recomputed from the first forward after every weight sync (inference side) or
+ * from a calibration subset (trainer side), then K/V are stored as FP8 E4M3.  Readings
+ * (K1-K4):
+ *   K1  calibration scale = O4 applied to the per-tensor amax over every calibration
+ *       element:  s = RN32(amax / 448), amax == 0 -> 1   (one scalar per layer and tensor);
+ *       several calibration batches: amax is the max over all of them (set-monotone).
+ *   K2  stored code = O5:  O2(RN32(x / s))   (the same element map as the weights).
+ *   K3  values beyond the calibrated range saturate (O2's +-448), and are COUNTED: an
+ *       element is saturated iff |RN32(x / s)| >= 464, i.e. iff the satfinite clamp
+ *       decides its code (464 is the midpoint between 448 and the next E4M3 binade's 480).
+ *   K4  append: token row r of the new K (or V) is written to cache row slot[r]
+ *       (slot = identity when no mapping is given).
+ */
+
+/* K1: amax over a BF16 [rows, cols] matrix (row stride ld), exact; returns 1 if any element
+ * is NaN/Inf (and leaves *amax undefined), else 0. */
+int oracle_kv_amax(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld, float* amax) {
+    float a = 0.0f;
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t c = 0; c < cols; ++c) {
+            float v = fabsf(oracle_bf16_to_float(x[r * ld + c]));
+            if (!isfinite(v)) return ORACLE_ENONFINITE;
+            if (v > a) a = v;
+        }
+    *amax = a;
+    return ORACLE_OK;
+}
+
+/* K2-K4: quantize rows of x with the scalar scale s into cache rows slot[r] (slot may be
+ * NULL = identity); returns the number of saturated elements (K3). */
+int64_t oracle_kv_quantize_append(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld, float s,
+                                  const int32_t* slot, uint8_t* cache, int64_t ld_cache) {
+    int64_t saturated = 0;
+    for (int64_t r = 0; r < rows; ++r) {
+        int64_t dst = slot ? (int64_t)slot[r] : r;
+        for (int64_t c = 0; c < cols; ++c) {
+            float v = oracle_bf16_to_float(x[r * ld + c]);
+            volatile float q = v / s;
+            if (fabsf(q) >= 464.0f) ++saturated;
+            cache[dst * ld_cache + c] = oracle_e4m3_encode(q);
+        }
+    }
+    return saturated;
+}
