@@ -14,10 +14,13 @@
 // xor-shuffle tree; inv = rsqrt_rn(mean + eps); y = RN(RN(x inv) gamma) -> BF16 RNE.
 // RMSNorm makes two passes over the row (the second hits L2), so HBM sees x once.
 // silu(g) = g * sigmoid(g) in an overflow-free form with approximate exp2 / reciprocal (see
-// silu(): a few binary32 ulps).  (The oracle evaluates the producers in
+// silu2(): a few binary32 ulps).  All element math runs on binary32 PAIRS (FMUL2 / FFMA2 /
+// FADD2: one instruction for two correctly rounded operations, packed.cuh) -- these kernels
+// are instruction-bound, not HBM-bound, with scalar math.  (The oracle evaluates the producers in
 // binary64; the two BF16 results agree except for rare ties, see tests/test_gpu_producers.py.)
 #include <cstdint>
 
+#include "packed.cuh"
 #include "ptx.cuh"
 #include "quant_kernels.h"
 #include "scale_tables.cuh"
@@ -36,27 +39,42 @@ __device__ __forceinline__ uint32_t absmax_bits8(const uint4& v) {
 __device__ __forceinline__ float scale_of(uint32_t ab) {
     return ab == 0u ? 1.0f : __fdiv_rn(__uint_as_float(ab << 16), 448.0f);
 }
-__device__ __forceinline__ float quot(float x, float s, float r, bool fast) {
-    if (!fast) return __fdiv_rn(x, s);
-    const float q0 = __fmul_rn(x, r);
-    const float e = __fmaf_rn(-q0, s, x);
-    return __fmaf_rn(e, r, q0);
-}
 // 8 BF16 (4 words) -> 8 codes (2 words); sign bits OR-ed in (restores -0, no-op otherwise).
-__device__ __forceinline__ uint2 encode8(const uint4& v, float s, float r, bool fast) {
+// Fast path: the pair Markstein quotient; slow path (amax < 2^-104 or non-finite): div.rn.
+__device__ __forceinline__ uint2 encode8_fast(const uint4& v, float s, float r) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    const uint64_t rr = pack2(r, r), nss = pack2(-s, -s);
+    uint32_t c[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
+        const uint64_t qa = quot2_fast(bf16x2_to_f32x2(wa), rr, nss);
+        const uint64_t qb = quot2_fast(bf16x2_to_f32x2(wb), rr, nss);
+        const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;
+        c[i] = (cvt_e4m3x2(lo_of(qa), hi_of(qa)) | (cvt_e4m3x2(lo_of(qb), hi_of(qb)) << 16)) | sign;
+    }
+    return make_uint2(c[0], c[1]);
+}
+__device__ __noinline__ uint2 encode8_slow(const uint4& v, float s) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     uint32_t c[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
-        const float q0 = quot(__uint_as_float(wa << 16), s, r, fast);
-        const float q1 = quot(__uint_as_float(wa & 0xFFFF0000u), s, r, fast);
-        const float q2 = quot(__uint_as_float(wb << 16), s, r, fast);
-        const float q3 = quot(__uint_as_float(wb & 0xFFFF0000u), s, r, fast);
+        const float q0 = __fdiv_rn(__uint_as_float(wa << 16), s);
+        const float q1 = __fdiv_rn(__uint_as_float(wa & 0xFFFF0000u), s);
+        const float q2 = __fdiv_rn(__uint_as_float(wb << 16), s);
+        const float q3 = __fdiv_rn(__uint_as_float(wb & 0xFFFF0000u), s);
         const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;
         c[i] = (cvt_e4m3x2(q0, q1) | (cvt_e4m3x2(q2, q3) << 16)) | sign;
     }
     return make_uint2(c[0], c[1]);
+}
+// The amax of this lane's half-warp group (lanes 0-15 / 16-31 hold one 128-channel group each).
+__device__ __forceinline__ uint32_t group_amax(uint32_t ab) {
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) ab = max(ab, __shfl_xor_sync(0xFFFFFFFFu, ab, off));
+    return ab;
 }
 // The group's scale (table path for the fast-path amax range, IEEE division otherwise), the
 // scale store by lane 0 of the half-warp, and the encode of this lane's 8 values.
@@ -72,12 +90,7 @@ __device__ __forceinline__ uint2 quantize8(const uint4& y, uint32_t ab, int lane
         *scale_dst = s;
         if (ab >= kNonFinite && flag != nullptr) *flag = 1;
     }
-    return encode8(y, s, r, fast);
-}
-__device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
-    uint32_t r;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));  // first source -> high half
-    return r;
+    return fast ? encode8_fast(y, s, r) : encode8_slow(y, s);
 }
 // silu(g) = g * sigmoid(g) without overflow: with e = exp(-|g|) (never overflows),
 // sigmoid = 1 / (1 + e) for g >= 0 and e / (1 + e) for g < 0.  exp via ex2.approx (no ftz:
@@ -93,10 +106,17 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ float silu(float g) {
-    const float e = ex2_approx(-fabsf(g) * 1.4426950408889634f);
-    const float r = rcp_approx(1.0f + e);
-    return g >= 0.0f ? g * r : (g * e) * r;
+__device__ __forceinline__ uint64_t silu2(uint64_t g2) {
+    const uint64_t a2 = g2 & 0x7FFFFFFF7FFFFFFFull;  // |g|
+    const uint64_t t2 = mul2(a2, pack2(-1.4426950408889634f, -1.4426950408889634f));
+    const float e0 = ex2_approx(lo_of(t2)), e1 = ex2_approx(hi_of(t2));
+    const uint64_t d2 = add2(pack2(e0, e1), pack2(1.0f, 1.0f));
+    const float r0 = rcp_approx(lo_of(d2)), r1 = rcp_approx(hi_of(d2));
+    const uint64_t er2 = mul2(pack2(e0, e1), pack2(r0, r1));
+    // sigmoid: r for g >= 0, e r for g < 0 (selected by the sign bit of g)
+    const float sg0 = (lo_of(g2) >= 0.0f) ? r0 : lo_of(er2);
+    const float sg1 = (hi_of(g2) >= 0.0f) ? r1 : hi_of(er2);
+    return mul2(g2, pack2(sg0, sg1));
 }
 __device__ __forceinline__ uint4 ld_nc(const void* p) {
     uint4 r;
@@ -124,40 +144,41 @@ __global__ void __launch_bounds__(256, 3) rmsnorm_quantize_kernel(
     const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
     const int T = static_cast<int>((k + 255) / 256);
     for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); row < m; row += warps) {
-        const uint16_t* xr = x + row * ld_x;
-        float ss = 0.0f;
+        const uint16_t* xr = x + row * ld_x + lane * 8;
+        // pass 1: sum of squares, two interleaved binary32 partial sums per lane (FFMA2)
+        uint64_t ss2 = 0;
         for (int t0 = 0; t0 < T; t0 += UNROLL) {
             uint4 v[UNROLL];
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
-                const int64_t col = int64_t(t0 + u) * 256 + lane * 8;
                 v[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (t0 + u < T && col < k) v[u] = *reinterpret_cast<const uint4*>(xr + col);
+                if (t0 + u < T && (t0 + u) * 256 + lane * 8 < k) v[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
             }
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
                 const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
-                    ss = __fmaf_rn(lo, lo, ss);
-                    ss = __fmaf_rn(hi, hi, ss);
+                    const uint64_t x2 = bf16x2_to_f32x2(w[i]);
+                    ss2 = fma2(x2, x2, ss2);
                 }
             }
         }
+        float ss = __fadd_rn(lo_of(ss2), hi_of(ss2));
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xFFFFFFFFu, ss, off);
         const float mean = __fdiv_rn(ss, static_cast<float>(k));
         const float inv = __frsqrt_rn(__fadd_rn(mean, eps));
+        const uint64_t inv2 = pack2(inv, inv);
         constexpr int U2 = 4;  // pass 2: U2 vectors of x and gamma loaded before any use
         for (int t0 = 0; t0 < T; t0 += U2) {
             uint4 xv[U2], gv[U2];
 #pragma unroll
             for (int u = 0; u < U2; ++u) {
-                const int64_t col = int64_t(t0 + u) * 256 + lane * 8;
+                const int col = (t0 + u) * 256 + lane * 8;
                 xv[u] = gv[u] = make_uint4(0u, 0u, 0u, 0u);
                 if (t0 + u < T && col < k) {
-                    xv[u] = *reinterpret_cast<const uint4*>(xr + col);
+                    xv[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
                     gv[u] = __ldg(reinterpret_cast<const uint4*>(gamma + col));
                 }
             }
@@ -165,26 +186,20 @@ __global__ void __launch_bounds__(256, 3) rmsnorm_quantize_kernel(
             for (int u = 0; u < U2; ++u) {
                 const int t = t0 + u;
                 if (t >= T) break;  // warp-uniform
-                const int64_t col = int64_t(t) * 256 + lane * 8;
-                const bool half_live = (int64_t(t) * 256 + (lane >> 4) * 128) < k;  // uniform per half
+                const int col = t * 256 + lane * 8;
+                const bool half_live = (t * 256 + (lane >> 4) * 128) < k;  // uniform per half
                 const uint32_t w[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
                 const uint32_t gw[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
                 uint32_t o[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float lo = __fmul_rn(__fmul_rn(__uint_as_float(w[i] << 16), inv), __uint_as_float(gw[i] << 16));
-                    const float hi = __fmul_rn(__fmul_rn(__uint_as_float(w[i] & 0xFFFF0000u), inv),
-                                               __uint_as_float(gw[i] & 0xFFFF0000u));
-                    o[i] = bf16x2(lo, hi);
-                }
-                uint4 y = make_uint4(o[0], o[1], o[2], o[3]);  // zeros past k (x and gamma were 0)
+                for (int i = 0; i < 4; ++i)  // y = RN(RN(x inv) gamma), rounded to BF16
+                    o[i] = f32x2_to_bf16x2(mul2(mul2(bf16x2_to_f32x2(w[i]), inv2), bf16x2_to_f32x2(gw[i])));
+                const uint4 y = make_uint4(o[0], o[1], o[2], o[3]);  // zeros past k (x and gamma were 0)
                 if (y_out != nullptr && col < k) st_v4(y_out + row * ld_y + col, y.x, y.y, y.z, y.w);
                 // the whole warp reduces (lanes of a dead half contribute zeros and store nothing)
-                uint32_t ab = absmax_bits8(y);
-#pragma unroll
-                for (int off = 8; off >= 1; off >>= 1) ab = max(ab, __shfl_xor_sync(0xFFFFFFFFu, ab, off));
+                const uint32_t ab = group_amax(absmax_bits8(y));
                 if (half_live) {
-                    const int64_t g = int64_t(t) * 2 + (lane >> 4);
+                    const int g = t * 2 + (lane >> 4);
                     const uint2 c = quantize8(y, ab, lane, scales + g * ld_s + row, flag, tabs);
                     st_stream_v2(q + row * ld_q + col, c.x, c.y);
                 }
@@ -193,9 +208,80 @@ __global__ void __launch_bounds__(256, 3) rmsnorm_quantize_kernel(
     }
 }
 
+// The same computation for k = 256 NV (every Qwen3 hidden size): all loops have compile-time
+// trip counts and no lane predicates (no divergence bookkeeping around the shuffles).
+// (Measured alternative: keeping the row in registers between the passes instead of
+// re-reading it from L2 halves the occupancy and is 20 % slower.)
+template <int NV>
+__global__ void __launch_bounds__(256, 3) rmsnorm_quantize_fixed_kernel(
+    const uint16_t* __restrict__ x, const uint16_t* __restrict__ gamma, float eps, int64_t m, int64_t ld_x,
+    uint8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scales, int64_t ld_s, uint16_t* __restrict__ y_out,
+    int64_t ld_y, int32_t* __restrict__ flag) {
+    constexpr int K = NV * 256;
+    constexpr int P1 = NV < 8 ? NV : 8;  // pass-1 loads in flight per lane
+    constexpr int U2 = NV < 4 ? NV : 4;  // pass-2 vectors (x and gamma) loaded before use
+    __shared__ ScaleTables tabs;
+    init_scale_tables(tabs);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
+    const uint16_t* gl = gamma + lane * 8;
+    for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); row < m; row += warps) {
+        const uint16_t* xr = x + row * ld_x + lane * 8;
+        uint8_t* qr = q + row * ld_q + lane * 8;
+        uint64_t ss2 = 0;
+#pragma unroll 1
+        for (int t0 = 0; t0 < NV; t0 += P1) {
+            uint4 v[P1];
+#pragma unroll
+            for (int u = 0; u < P1; ++u) v[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
+#pragma unroll
+            for (int u = 0; u < P1; ++u) {
+                const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint64_t x2 = bf16x2_to_f32x2(w[i]);
+                    ss2 = fma2(x2, x2, ss2);
+                }
+            }
+        }
+        float ss = __fadd_rn(lo_of(ss2), hi_of(ss2));
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xFFFFFFFFu, ss, off);
+        const float inv = __frsqrt_rn(__fadd_rn(__fdiv_rn(ss, static_cast<float>(K)), eps));
+        const uint64_t inv2 = pack2(inv, inv);
+#pragma unroll 1
+        for (int t0 = 0; t0 < NV; t0 += U2) {
+            uint4 xv[U2], gv[U2];
+#pragma unroll
+            for (int u = 0; u < U2; ++u) {
+                xv[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
+                gv[u] = __ldg(reinterpret_cast<const uint4*>(gl + (t0 + u) * 256));
+            }
+#pragma unroll
+            for (int u = 0; u < U2; ++u) {
+                const int t = t0 + u;
+                const uint32_t w[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+                const uint32_t gw[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+                uint32_t o[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)  // y = RN(RN(x inv) gamma), rounded to BF16
+                    o[i] = f32x2_to_bf16x2(mul2(mul2(bf16x2_to_f32x2(w[i]), inv2), bf16x2_to_f32x2(gw[i])));
+                const uint4 y = make_uint4(o[0], o[1], o[2], o[3]);
+                if (y_out != nullptr) st_v4(y_out + row * ld_y + t * 256 + lane * 8, y.x, y.y, y.z, y.w);
+                const uint32_t ab = group_amax(absmax_bits8(y));
+                const int g = t * 2 + (lane >> 4);
+                const uint2 c = quantize8(y, ab, lane, scales + g * ld_s + row, flag, tabs);
+                st_stream_v2(qr + t * 256, c.x, c.y);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // SiLU(gate) * up + quantize: one warp per (token row, chunk of 8 output groups); vector j of
 // lane l covers outputs chunk*1024 + 256 j + 8 l .. +7 (group 2j + (l >= 16)).
+template <bool FULL>
 __global__ void __launch_bounds__(256) silu_mul_quantize_kernel(
     const uint16_t* __restrict__ gu, int64_t m, int64_t inter, int64_t ld_gu, uint8_t* __restrict__ q,
     int64_t ld_q, float* __restrict__ scales, int64_t ld_s, uint16_t* __restrict__ y_out, int64_t ld_y,
@@ -206,42 +292,35 @@ __global__ void __launch_bounds__(256) silu_mul_quantize_kernel(
     const int lane = threadIdx.x & 31;
     const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (item >= m * chunks) return;
-    const int64_t row = item / chunks, chunk = item - (item / chunks) * chunks;
-    const int64_t groups = inter >> 7;
-    const uint16_t* gr = gu + row * ld_gu;
+    const int64_t row = item / chunks;
+    const int chunk = static_cast<int>(item - row * chunks);
+    const int groups = static_cast<int>(inter >> 7);
+    const uint16_t* gr = gu + row * ld_gu + (lane & 15) * 8;
     uint4 gv[4], uv[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int64_t g = chunk * 8 + 2 * j + (lane >> 4);
+        const int g = chunk * 8 + 2 * j + (lane >> 4);
         gv[j] = uv[j] = make_uint4(0u, 0u, 0u, 0u);
-        if (g < groups) {
-            const int64_t col = g * 128 + (lane & 15) * 8;
-            gv[j] = ld_nc(gr + col);
-            uv[j] = ld_nc(gr + inter + col);
+        if (FULL || g < groups) {
+            gv[j] = ld_nc(gr + g * 128);
+            uv[j] = ld_nc(gr + inter + g * 128);
         }
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int64_t g = chunk * 8 + 2 * j + (lane >> 4);
+        const int g = chunk * 8 + 2 * j + (lane >> 4);
         const uint32_t gw[4] = {gv[j].x, gv[j].y, gv[j].z, gv[j].w};
         const uint32_t uw[4] = {uv[j].x, uv[j].y, uv[j].z, uv[j].w};
         uint32_t o[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float g0 = __uint_as_float(gw[i] << 16), g1 = __uint_as_float(gw[i] & 0xFFFF0000u);
-            const float u0 = __uint_as_float(uw[i] << 16), u1 = __uint_as_float(uw[i] & 0xFFFF0000u);
-            const float s0 = silu(g0);
-            const float s1 = silu(g1);
-            o[i] = bf16x2(__fmul_rn(s0, u0), __fmul_rn(s1, u1));
-        }
+        for (int i = 0; i < 4; ++i)  // y = RN(silu(g) u), rounded to BF16
+            o[i] = f32x2_to_bf16x2(mul2(silu2(bf16x2_to_f32x2(gw[i])), bf16x2_to_f32x2(uw[i])));
         const uint4 y = make_uint4(o[0], o[1], o[2], o[3]);
-        uint32_t ab = absmax_bits8(y);
-#pragma unroll
-        for (int off = 8; off >= 1; off >>= 1) ab = max(ab, __shfl_xor_sync(0xFFFFFFFFu, ab, off));
-        if (g < groups) {
-            const int64_t col = g * 128 + (lane & 15) * 8;
+        const uint32_t ab = group_amax(absmax_bits8(y));
+        if (FULL || g < groups) {
+            const int col = g * 128 + (lane & 15) * 8;
             if (y_out != nullptr) st_v4(y_out + row * ld_y + col, y.x, y.y, y.z, y.w);
-            const uint2 c = quantize8(y, ab, lane, scales + g * ld_s + row, flag, tabs);
+            const uint2 c = quantize8(y, ab, lane, scales + int64_t(g) * ld_s + row, flag, tabs);
             st_stream_v2(q + row * ld_q + col, c.x, c.y);
         }
     }
@@ -263,8 +342,22 @@ cudaError_t launch_rmsnorm_quantize(const uint16_t* x, const uint16_t* gamma, fl
                                     uint16_t* y, int64_t ld_y, int32_t* flag, cudaStream_t stream) {
     if (m == 0 || k == 0) return cudaSuccess;
     const int64_t rows_blocks = (m + 7) / 8;
-    const int64_t cap = 4LL * sms();
+    const int64_t cap = 3LL * sms();
     const unsigned grid = static_cast<unsigned>(rows_blocks < cap ? rows_blocks : cap);
+    if (k % 256 == 0 && k <= 4096) {
+        switch (k / 256) {
+#define RMS_FIXED(NV)                                                                                      \
+    case NV:                                                                                               \
+        rmsnorm_quantize_fixed_kernel<NV><<<grid, 256, 0, stream>>>(x, gamma, eps, m, ld_x, q, ld_q, scales, \
+                                                                    ld_s, y, ld_y, flag);                  \
+        return cudaGetLastError();
+            RMS_FIXED(1) RMS_FIXED(2) RMS_FIXED(3) RMS_FIXED(4) RMS_FIXED(5) RMS_FIXED(6) RMS_FIXED(7)
+            RMS_FIXED(8) RMS_FIXED(9) RMS_FIXED(10) RMS_FIXED(11) RMS_FIXED(12) RMS_FIXED(13) RMS_FIXED(14)
+            RMS_FIXED(15) RMS_FIXED(16)
+#undef RMS_FIXED
+            default: break;
+        }
+    }
     rmsnorm_quantize_kernel<<<grid, 256, 0, stream>>>(x, gamma, eps, m, k, ld_x, q, ld_q, scales, ld_s, y, ld_y, flag);
     return cudaGetLastError();
 }
@@ -277,8 +370,12 @@ cudaError_t launch_silu_mul_quantize(const uint16_t* gu, int64_t m, int64_t inte
     const int64_t items = m * chunks;
     const int64_t blocks = (items + 7) / 8;
     if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
-    silu_mul_quantize_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(gu, m, inter, ld_gu, q, ld_q, scales,
-                                                                               ld_s, y, ld_y, chunks, flag);
+    if ((inter / 128) % 8 == 0)
+        silu_mul_quantize_kernel<true><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+            gu, m, inter, ld_gu, q, ld_q, scales, ld_s, y, ld_y, chunks, flag);
+    else
+        silu_mul_quantize_kernel<false><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+            gu, m, inter, ld_gu, q, ld_q, scales, ld_s, y, ld_y, chunks, flag);
     return cudaGetLastError();
 }
 

@@ -21,6 +21,7 @@
 
 #include "ptx.cuh"
 #include "quant_kernels.h"
+#include "packed.cuh"
 #include "scale_tables.cuh"
 
 namespace fp8q {
@@ -204,20 +205,6 @@ __device__ __forceinline__ uint32_t abs_max_bits16(const uint32_t (&w)[8]) {
     uint32_t a = __vmaxu2(__vmaxu2(__vmaxu2(w[0] & m, w[1] & m), __vmaxu2(w[2] & m, w[3] & m)),
                           __vmaxu2(__vmaxu2(w[4] & m, w[5] & m), __vmaxu2(w[6] & m, w[7] & m)));
     return max(a & 0xFFFFu, a >> 16);
-}
-__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
-    return (static_cast<uint64_t>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
-}
-__device__ __forceinline__ float lo_of(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
-__device__ __forceinline__ float hi_of(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
-// (x0, x1) -> (RN32(x0 / s), RN32(x1 / s)) for blocks with amax >= 2^-104 (see header);
-// rr = (r, r), nss = (-s, -s).  The sign of a zero quotient is fixed later (sign OR).
-__device__ __forceinline__ uint64_t quot2_fast(uint64_t x, uint64_t rr, uint64_t nss) {
-    uint64_t q0, e, q1;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(q0) : "l"(x), "l"(rr));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(q0), "l"(nss), "l"(x));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(q1) : "l"(e), "l"(rr), "l"(q0));
-    return q1;
 }
 // 16 BF16 (8 words) -> 16 E4M3 codes (4 words).
 template <bool kFast>
