@@ -199,6 +199,49 @@ fp8q_status fp8_block_gemm_grouped(const uint8_t* a, int64_t ld_a, const float* 
                                    int32_t num_groups, void* workspace, size_t workspace_bytes,
                                    void* stream);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT-3: FP8 KV cache with per-step scale recalibration (§2.3.1:
+ * "we trigger a forced recalibration ... before the rollout phase of each RL step" (inference
+ * side) / "recalibrates QKV scales using the updated policy weights and a subset of training
+ * data" (trainer side)).  One scalar scale per layer and tensor (K, V, Q):
+ *   calibration   amax = max |x| over every calibration element (all batches),
+ *                 scale = RN32(amax / 448), amax == 0 -> 1            (readings K1, Q4, Q5)
+ *   append        cache[slot[r]][c] = E4M3_RNE_sat(RN32(x[r][c] / scale))   (K2, K4; O5)
+ *   saturation    an element saturates iff |RN32(x / scale)| >= 464 (its code is then +-448);
+ *                 such elements are counted                                    (K3)
+ * Layout: x is BF16 [rows = tokens, cols = heads * head_dim] with row stride ld_x elements;
+ * the cache is uint8 [num_slots][ld_cache].  All pointers are device pointers owned by the
+ * caller; everything is enqueued on `stream`; no host sync.
+ * ------------------------------------------------------------------------------------------ */
+
+/*
+ * kv_amax_update -- *amax_bits = max(*amax_bits, BF16 bits of max |x|) (sign-cleared BF16 bits
+ *   in a uint32; the caller zeroes it to start a calibration = "reset calculate_kv_scales").
+ *   Deterministic (an integer max).  flag (nullable): bit 0 set if x holds NaN/Inf.
+ *   Errors: negative sizes or ld_x < cols (EINVAL); misaligned pointers (EALIGN).
+ */
+fp8q_status kv_amax_update(const void* x_bf16, int64_t rows, int64_t cols, int64_t ld_x, uint32_t* amax_bits,
+                           int32_t* flag, void* stream);
+
+/*
+ * kv_scale_from_amax -- scales[i] = RN32(amax_i / 448) (amax_i == 0 -> 1) for count layers /
+ *   tensors at once; amax_bits as written by kv_amax_update.
+ */
+fp8q_status kv_scale_from_amax(const uint32_t* amax_bits, int64_t count, float* scales, void* stream);
+
+/*
+ * kv_quantize_append -- writes the E4M3 codes of x's rows into cache rows slots[r] (slots
+ *   nullable: row r -> cache row r, then rows <= num_slots is required (ESHAPE)), with the
+ *   scalar *scale (device).  saturated (nullable): += number of saturated elements.  flag
+ *   (nullable): |= 1 if x holds NaN/Inf (those codes unspecified), |= 2 if a slot is outside
+ *   [0, num_slots) (that row is skipped).  Rows must not map to the same slot twice.
+ *   Errors: EINVAL (sizes, ld_x < cols, ld_cache < cols, null x/scale/cache), EALIGN.
+ *   Traffic: 2 B read + 1 B written per element (HBM-bound).
+ */
+fp8q_status kv_quantize_append(const void* x_bf16, int64_t rows, int64_t cols, int64_t ld_x, const float* scale,
+                               const int32_t* slots, uint8_t* cache, int64_t ld_cache, int64_t num_slots,
+                               uint32_t* saturated, int32_t* flag, void* stream);
+
 /*
  * fp8q_kernel_launches -- number of kernels this library has launched in this process
  * (monotone counter; used by bench.py to report `gpu_launches`).

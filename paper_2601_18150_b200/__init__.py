@@ -10,6 +10,9 @@ from .fp8q import (  # noqa: F401
     fp8_block_gemm,
     fp8_block_gemm_grouped,
     kernel_launches,
+    kv_amax_update,
+    kv_quantize_append,
+    kv_scale_from_amax,
     load_library,
     quantize_act_per_token_group,
     quantize_weight_blockwise,

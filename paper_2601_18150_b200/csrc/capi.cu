@@ -182,6 +182,51 @@ fp8q_status silu_mul_quantize_act_per_token_group(const void* gate_up_bf16, int6
     return from_cuda(e);
 }
 
+fp8q_status kv_amax_update(const void* x_bf16, int64_t rows, int64_t cols, int64_t ld_x, uint32_t* amax_bits,
+                           int32_t* flag, void* stream) {
+    if (rows < 0 || cols < 0 || ld_x < cols) return FP8Q_EINVAL;
+    if (rows == 0 || cols == 0) return FP8Q_OK;
+    if (x_bf16 == nullptr || amax_bits == nullptr) return FP8Q_EINVAL;
+    if (!aligned(x_bf16, 2) || !aligned(amax_bits, 4) || !aligned(flag, 4)) return FP8Q_EALIGN;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_kv_amax(static_cast<const uint16_t*>(x_bf16), rows, cols, ld_x, amax_bits, flag,
+                                         static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
+fp8q_status kv_scale_from_amax(const uint32_t* amax_bits, int64_t count, float* scales, void* stream) {
+    if (count < 0) return FP8Q_EINVAL;
+    if (count == 0) return FP8Q_OK;
+    if (amax_bits == nullptr || scales == nullptr) return FP8Q_EINVAL;
+    if (!aligned(amax_bits, 4) || !aligned(scales, 4)) return FP8Q_EALIGN;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_kv_scale(amax_bits, count, scales, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
+fp8q_status kv_quantize_append(const void* x_bf16, int64_t rows, int64_t cols, int64_t ld_x, const float* scale,
+                               const int32_t* slots, uint8_t* cache, int64_t ld_cache, int64_t num_slots,
+                               uint32_t* saturated, int32_t* flag, void* stream) {
+    if (rows < 0 || cols < 0 || ld_x < cols || ld_cache < cols || num_slots < 0) return FP8Q_EINVAL;
+    if (slots == nullptr && rows > num_slots) return FP8Q_ESHAPE;
+    if (rows == 0 || cols == 0) return FP8Q_OK;
+    if (x_bf16 == nullptr || scale == nullptr || cache == nullptr) return FP8Q_EINVAL;
+    if (!aligned(x_bf16, 2) || !aligned(scale, 4) || !aligned(slots, 4) || !aligned(saturated, 4) ||
+        !aligned(flag, 4))
+        return FP8Q_EALIGN;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_kv_append(static_cast<const uint16_t*>(x_bf16), rows, cols, ld_x, scale, slots,
+                                           cache, ld_cache, num_slots, saturated, flag,
+                                           static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
 size_t fp8_block_gemm_workspace_size(int64_t m, int64_t n, int64_t k) {
     return fp8q::gemm_workspace_bytes(m, n, k, false);
 }

@@ -71,6 +71,14 @@ cudaError_t launch_silu_mul_quantize(const uint16_t* gu, int64_t m, int64_t inte
                                      int64_t ld_q, float* scales, int64_t ld_s, uint16_t* y, int64_t ld_y,
                                      int32_t* flag, cudaStream_t stream);
 
+// NEXT-3 FP8 KV cache (kv.cu).
+cudaError_t launch_kv_amax(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld, uint32_t* amax_bits,
+                           int32_t* flag, cudaStream_t stream);
+cudaError_t launch_kv_scale(const uint32_t* amax_bits, int64_t n, float* scales, cudaStream_t stream);
+cudaError_t launch_kv_append(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld_x, const float* scale,
+                             const int32_t* slots, uint8_t* cache, int64_t ld_c, int64_t num_slots,
+                             uint32_t* saturated, int32_t* flag, cudaStream_t stream);
+
 // Dev-only: record a pipeline timeline of CTA 0 into dev_ptr (96 k-blocks x 12 uint32 clocks).
 void set_gemm_trace(uint32_t* dev_ptr);
 uint32_t* get_gemm_trace();

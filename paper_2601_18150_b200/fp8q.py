@@ -74,6 +74,12 @@ def load_library() -> ctypes.CDLL:
                                                ctypes.c_int, I64, I64, I64, P, I32, P,
                                                ctypes.c_size_t, P]
         lib.fp8_block_gemm_grouped.restype = ctypes.c_int
+        lib.kv_amax_update.argtypes = [P, I64, I64, I64, P, P, P]
+        lib.kv_amax_update.restype = ctypes.c_int
+        lib.kv_scale_from_amax.argtypes = [P, I64, P, P]
+        lib.kv_scale_from_amax.restype = ctypes.c_int
+        lib.kv_quantize_append.argtypes = [P, I64, I64, I64, P, P, P, I64, I64, P, P, P]
+        lib.kv_quantize_append.restype = ctypes.c_int
         _lib = lib
         return lib
 
@@ -319,3 +325,54 @@ def fp8_block_gemm_grouped(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Ten
         FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16, m, n, k, offsets.data_ptr(),
         G, None, 0, _stream(stream)), "fp8_block_gemm_grouped")
     return out
+
+
+# ------------------------------------------------------------------ NEXT-3 FP8 KV cache
+def _opt_ptr(t, name, dtype):
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype == dtype):
+        raise Fp8qError(f"{name} must be a CUDA {dtype} tensor")
+    return t.data_ptr()
+
+
+def kv_amax_update(x: torch.Tensor, amax_bits: torch.Tensor, flag: torch.Tensor | None = None, stream=None):
+    """amax_bits (int32 [1] on the device, BF16 bits) = max(amax_bits, max |x|)."""
+    _cuda2d(x, "x", torch.bfloat16)
+    ap = _opt_ptr(amax_bits, "amax_bits", torch.int32)
+    if ap is None:
+        raise Fp8qError("amax_bits is required")
+    _check(load_library().kv_amax_update(x.data_ptr(), x.shape[0], x.shape[1], _ld(x), ap,
+                                         _opt_ptr(flag, "flag", torch.int32), _stream(stream)), "kv_amax_update")
+    return amax_bits
+
+
+def kv_scale_from_amax(amax_bits: torch.Tensor, scales: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """scales[i] = RN32(amax_i / 448), amax 0 -> 1, for every entry of amax_bits (int32)."""
+    if not (amax_bits.is_cuda and amax_bits.dtype == torch.int32 and amax_bits.is_contiguous()):
+        raise Fp8qError("amax_bits must be a contiguous CUDA int32 tensor")
+    if scales is None:
+        scales = torch.empty(amax_bits.shape, dtype=torch.float32, device=amax_bits.device)
+    _check(load_library().kv_scale_from_amax(amax_bits.data_ptr(), amax_bits.numel(),
+                                             _opt_ptr(scales, "scales", torch.float32), _stream(stream)),
+           "kv_scale_from_amax")
+    return scales
+
+
+def kv_quantize_append(x: torch.Tensor, scale: torch.Tensor, cache: torch.Tensor, slots: torch.Tensor | None = None,
+                       saturated: torch.Tensor | None = None, flag: torch.Tensor | None = None, stream=None):
+    """cache[slots[r]] = E4M3 codes of x[r] / scale (scale: CUDA float32 scalar tensor);
+    saturated (int32 [1]) accumulates the saturated-element count."""
+    _cuda2d(x, "x", torch.bfloat16)
+    _cuda2d(cache, "cache", torch.uint8)
+    if not (scale.is_cuda and scale.dtype == torch.float32 and scale.numel() >= 1):
+        raise Fp8qError("scale must be a CUDA float32 tensor")
+    if slots is not None and not (slots.is_cuda and slots.dtype == torch.int32 and slots.is_contiguous()
+                                  and slots.numel() == x.shape[0]):
+        raise Fp8qError("slots must be a contiguous CUDA int32 tensor with one entry per row of x")
+    _check(load_library().kv_quantize_append(
+        x.data_ptr(), x.shape[0], x.shape[1], _ld(x), scale.data_ptr(),
+        slots.data_ptr() if slots is not None else None, cache.data_ptr(), _ld(cache), cache.shape[0],
+        _opt_ptr(saturated, "saturated", torch.int32), _opt_ptr(flag, "flag", torch.int32), _stream(stream)),
+        "kv_quantize_append")
+    return cache

@@ -32,7 +32,9 @@ def test_header_declares_the_boundary():
     for required in ["quantize_weight_blockwise", "quantize_act_per_token_group", "fp8_block_gemm",
                      "fp8_block_gemm_grouped", "fp8_block_gemm_workspace_size",
                      "fp8_block_gemm_grouped_workspace_size", "fp8q_status_string", "fp8q_version",
-                     "fp8q_kernel_launches"]:
+                     "fp8q_kernel_launches", "rmsnorm_quantize_act_per_token_group",
+                     "silu_mul_quantize_act_per_token_group", "kv_amax_update", "kv_scale_from_amax",
+                     "kv_quantize_append"]:
         assert required in names
 
 
@@ -72,6 +74,15 @@ def test_validation_paths_without_gpu(lib):
     assert lib.fp8_block_gemm_grouped(fake, 128, fake, 4, fake, 128, 2048, fake, 1, 1, fake, 16, 0,
                                       4, 16, 128, fake, -1, None, 0, None) == 2
     assert lib.fp8_block_gemm_workspace_size(8192, 6144, 4096) == 0  # prefill: no split-K
+    # NEXT-3 KV cache: ld < cols -> EINVAL; identity slots with rows > num_slots -> ESHAPE;
+    # misaligned amax / scale -> EALIGN; empty -> OK
+    assert lib.kv_amax_update(fake, 4, 1024, 512, fake, None, None) == 1
+    assert lib.kv_amax_update(fake, 4, 1024, 1024, odd, None, None) == 3
+    assert lib.kv_amax_update(None, 0, 1024, 1024, None, None, None) == 0
+    assert lib.kv_scale_from_amax(fake, -1, fake, None) == 1
+    assert lib.kv_quantize_append(fake, 8, 1024, 1024, fake, None, fake, 1024, 4, None, None, None) == 2
+    assert lib.kv_quantize_append(fake, 8, 1024, 1024, odd, fake, fake, 1024, 4, None, None, None) == 3
+    assert lib.kv_quantize_append(fake, 8, 1024, 1024, fake, fake, fake, 512, 16, None, None, None) == 1
 
 
 def test_product_package_never_imports_oracle():

@@ -55,7 +55,8 @@ def timeit(fn, iters, flush):
 def graph_time(fn, w, min_bytes=400 << 20):
     """Steady-state time per launch: a CUDA graph of back-to-back launches, each on its own
     copy of the weights (copies together > L2, so every launch streams from HBM)."""
-    copies = [w] + [w.clone() for _ in range(max(1, -(-min_bytes // w.numel())) - 1)]
+    nbytes = w.numel() * w.element_size()
+    copies = [w] + [w.clone() for _ in range(min(64, max(1, -(-min_bytes // nbytes))) - 1)]
     launches = 4 * len(copies)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
@@ -134,6 +135,25 @@ def main():
                     rec.update({"graph_ms": round(tg, 4), "graph_GBps": round(by / (tg * 1e-3) / 1e9, 1),
                                 "graph_frac_hbm": round(by / (tg * 1e-3) / 1e9 / HBM, 4)})
                 print(json.dumps(rec))
+    if args.what in ("all", "kv"):
+        # NEXT-3: calibration amax (2 B/elem) and append (3 B/elem) on Qwen3-8B K (8 heads x 128)
+        cols = 8 * 128
+        for T in (8192, 512, 64):
+            x = torch.randn((T, cols), generator=g, device=dev).to(torch.bfloat16)
+            amax = torch.zeros(1, dtype=torch.int32, device=dev)
+            t, lo, hi = timeit(lambda: fp8q.kv_amax_update(x, amax), args.iters, flush)
+            tg = graph_time(lambda xx: fp8q.kv_amax_update(xx, amax), x)
+            print(json.dumps({"kernel": "kv_amax_update", "shape": [T, cols], "ms": round(t, 4),
+                              "GBps": round(2 * T * cols / (t * 1e-3) / 1e9, 1), "graph_ms": round(tg, 4),
+                              "graph_frac_hbm": round(2 * T * cols / (tg * 1e-3) / 1e9 / HBM, 4)}))
+            scale = fp8q.kv_scale_from_amax(amax)
+            cache = torch.empty((T + 64, cols), dtype=torch.uint8, device=dev)
+            slots = torch.randperm(T + 64, device=dev)[:T].to(torch.int32)
+            t, lo, hi = timeit(lambda: fp8q.kv_quantize_append(x, scale, cache, slots), args.iters, flush)
+            tg = graph_time(lambda xx: fp8q.kv_quantize_append(xx, scale, cache, slots), x)
+            print(json.dumps({"kernel": "kv_quantize_append", "shape": [T, cols], "ms": round(t, 4),
+                              "GBps": round(3 * T * cols / (t * 1e-3) / 1e9, 1), "graph_ms": round(tg, 4),
+                              "graph_frac_hbm": round(3 * T * cols / (tg * 1e-3) / 1e9 / HBM, 4)}))
     if args.what in ("all", "prod"):
         M = 8192
         for k in (4096, 2048):
