@@ -195,12 +195,42 @@ class LayerStep:
                               out=self.y[name])
 
     def run_e2e(self):
-        for name in self.w:
-            self.w[name].copy_(self.h_w[name], non_blocking=True)
-            self.x[name].copy_(self.h_x[name], non_blocking=True)
-        self.run()
-        for name in self.y:
-            self.h_y[name].copy_(self.y[name], non_blocking=True)
+        """The step through the same C-ABI calls with host (pinned) inputs and outputs: H2D on
+        one copy stream (weights first, then each GEMM's activations), D2H of each GEMM's
+        output on another as soon as it is produced -- PCIe is full duplex, so the output
+        read-back overlaps the remaining input uploads and the compute."""
+        fq = self.fp8q
+        cur = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_h2d"):
+            self._h2d = torch.cuda.Stream(self.device)
+            self._d2h = torch.cuda.Stream(self.device)
+        h2d, d2h = self._h2d, self._d2h
+        h2d.wait_stream(cur)
+        ev_x = {}
+        with torch.cuda.stream(h2d):
+            for name in self.w:
+                self.w[name].copy_(self.h_w[name], non_blocking=True)
+            ev_w = torch.cuda.Event()
+            ev_w.record(h2d)
+            for name in self.x:
+                self.x[name].copy_(self.h_x[name], non_blocking=True)
+                ev_x[name] = torch.cuda.Event()
+                ev_x[name].record(h2d)
+        cur.wait_event(ev_w)
+        self.step_id += 1
+        self.engine.sync_step(self.step_id, self.w, self.comm)
+        for name, _, _ in LAYER:
+            cur.wait_event(ev_x[name])
+            fq.quantize_act_per_token_group(self.x[name], self.xq[name], self.xs[name])
+            fq.fp8_block_gemm(self.xq[name], self.xs[name], self.engine.codes[name], self.engine.scales[name],
+                              out=self.y[name])
+            ev_y = torch.cuda.Event()
+            ev_y.record(cur)
+            d2h.wait_event(ev_y)
+            with torch.cuda.stream(d2h):
+                self.h_y[name].copy_(self.y[name], non_blocking=True)
+        cur.wait_stream(d2h)
+        cur.wait_stream(h2d)
 
     def h2d_bytes(self):
         return sum(v.numel() * 2 for v in self.h_w.values()) + sum(v.numel() * 2 for v in self.h_x.values())

@@ -42,30 +42,29 @@ __global__ void __launch_bounds__(256) kv_amax_kernel(const uint16_t* __restrict
     uint32_t a = 0;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (vec) {  // 8 BF16 per thread per step (cols % 8 == 0, 16-byte aligned rows), KU loads in flight
+    // one warp per row (rows strided over the grid's warps): no per-element index division
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    (void)stride;
+    (void)tid;
+    if (vec) {  // 8 BF16 per lane per vector (cols % 8 == 0, 16-byte aligned rows), KU in flight
         constexpr int KU = 4;
-        const int64_t cv = cols / 8;
-        const int64_t total = rows * cv;
-        for (int64_t i0 = tid; i0 < total; i0 += stride * KU) {
-            uint4 v[KU];
+        const int cv = static_cast<int>(cols / 8);
+        for (int64_t r = w0; r < rows; r += nwarps) {
+            const uint4* xr = reinterpret_cast<const uint4*>(x + r * ld);
+            for (int c0 = lane; c0 < cv; c0 += 32 * KU) {
+                uint4 v[KU];
 #pragma unroll
-            for (int u = 0; u < KU; ++u) {
-                const int64_t i = i0 + u * stride;
-                v[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (i < total) {
-                    const int64_t r = i / cv, c = (i - r * cv) * 8;
-                    v[u] = __ldcs(reinterpret_cast<const uint4*>(x + r * ld + c));
-                }
+                for (int u = 0; u < KU; ++u)
+                    v[u] = (c0 + 32 * u < cv) ? __ldcs(xr + c0 + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (int u = 0; u < KU; ++u) a = max(a, amax_bits8(v[u]));
             }
-#pragma unroll
-            for (int u = 0; u < KU; ++u) a = max(a, amax_bits8(v[u]));
         }
     } else {
-        const int64_t total = rows * cols;
-        for (int64_t i = tid; i < total; i += stride) {
-            const int64_t r = i / cols, c = i - r * cols;
-            a = max(a, static_cast<uint32_t>(x[r * ld + c] & 0x7FFFu));
-        }
+        for (int64_t r = w0; r < rows; r += nwarps)
+            for (int64_t c = lane; c < cols; c += 32) a = max(a, static_cast<uint32_t>(x[r * ld + c] & 0x7FFFu));
     }
     a = __reduce_max_sync(0xFFFFFFFFu, a);
     if ((threadIdx.x & 31) == 0 && a != 0) {
@@ -127,54 +126,50 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const uint16_t* __restri
     uint32_t sat = 0, bad = 0;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (vec) {  // KU vectors of 8 BF16 loaded per thread before any is encoded
+    // one warp per row (rows strided over the grid's warps): no per-element index division
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    (void)stride;
+    (void)tid;
+    if (vec) {  // KU vectors of 8 BF16 loaded per lane before any is encoded
         constexpr int KU = 4;
-        const int64_t cv = cols / 8;
-        const int64_t total = rows * cv;
-        for (int64_t i0 = tid; i0 < total; i0 += stride * KU) {
-            uint4 v[KU];
-            int64_t dst[KU], col[KU];
+        const int cv = static_cast<int>(cols / 8);
+        for (int64_t row = w0; row < rows; row += nwarps) {
+            const int64_t dst = slots != nullptr ? slots[row] : row;
+            const uint4* xr = reinterpret_cast<const uint4*>(x + row * ld_x);
+            const bool ok = dst >= 0 && dst < num_slots;
+            bad |= ok ? 0u : 2u;
+            uint8_t* cr = cache + (ok ? dst : 0) * ld_c;
+            for (int c0 = lane; c0 < cv; c0 += 32 * KU) {
+                uint4 v[KU];
 #pragma unroll
-            for (int u = 0; u < KU; ++u) {
-                const int64_t i = i0 + u * stride;
-                v[u] = make_uint4(0u, 0u, 0u, 0u);
-                dst[u] = -1;
-                col[u] = 0;
-                if (i < total) {
-                    const int64_t row = i / cv;
-                    col[u] = (i - row * cv) * 8;
-                    dst[u] = slots != nullptr ? slots[row] : row;
-                    v[u] = __ldcs(reinterpret_cast<const uint4*>(x + row * ld_x + col[u]));
-                    if (dst[u] < 0 || dst[u] >= num_slots) {
-                        bad |= 2u;
-                        dst[u] = -1;
-                    }
+                for (int u = 0; u < KU; ++u)
+                    v[u] = (c0 + 32 * u < cv) ? __ldcs(xr + c0 + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (int u = 0; u < KU; ++u) {
+                    bad |= amax_bits8(v[u]) >= kKvNonFinite ? 1u : 0u;
+                    if (!ok || c0 + 32 * u >= cv) continue;
+                    const uint2 code = fast ? kv_encode8<true>(v[u], s, r, sat) : kv_encode8<false>(v[u], s, r, sat);
+                    st_stream_v2(cr + (c0 + 32 * u) * 8, code.x, code.y);
                 }
-            }
-#pragma unroll
-            for (int u = 0; u < KU; ++u) {
-                bad |= amax_bits8(v[u]) >= kKvNonFinite ? 1u : 0u;
-                if (dst[u] < 0) continue;
-                const uint2 code = fast ? kv_encode8<true>(v[u], s, r, sat) : kv_encode8<false>(v[u], s, r, sat);
-                st_stream_v2(cache + dst[u] * ld_c + col[u], code.x, code.y);
             }
         }
     } else {
-        const int64_t total = rows * cols;
-        for (int64_t i = tid; i < total; i += stride) {
-            const int64_t row = i / cols, c = i - row * cols;
+        for (int64_t row = w0; row < rows; row += nwarps) {
             const int64_t dst = slots != nullptr ? slots[row] : row;
-            const uint16_t h = x[row * ld_x + c];
-            bad |= (h & 0x7FFFu) >= kKvNonFinite ? 1u : 0u;
-            if (dst < 0 || dst >= num_slots) {
-                bad |= 2u;
-                continue;
+            const bool ok = dst >= 0 && dst < num_slots;
+            bad |= ok ? 0u : 2u;
+            for (int64_t c = lane; c < cols; c += 32) {
+                const uint16_t h = x[row * ld_x + c];
+                bad |= (h & 0x7FFFu) >= kKvNonFinite ? 1u : 0u;
+                if (!ok) continue;
+                const float q = __fdiv_rn(__uint_as_float(static_cast<uint32_t>(h) << 16), s);
+                const bool o = !(fabsf(q) < 464.0f);
+                sat += o ? 1u : 0u;
+                const uint32_t code = cvt_e4m3x2(o ? 448.0f : fabsf(q), 0.0f) & 0x7Fu;  // lo -> byte 0
+                cache[dst * ld_c + c] = static_cast<uint8_t>(code | ((h >> 8) & 0x80u));
             }
-            const float q = __fdiv_rn(__uint_as_float(static_cast<uint32_t>(h) << 16), s);
-            const bool o = !(fabsf(q) < 464.0f);
-            sat += o ? 1u : 0u;
-            const uint32_t code = cvt_e4m3x2(o ? 448.0f : fabsf(q), 0.0f) & 0x7Fu;  // lo -> byte 0
-            cache[dst * ld_c + c] = static_cast<uint8_t>(code | ((h >> 8) & 0x80u));
         }
     }
     sat = __reduce_add_sync(0xFFFFFFFFu, sat);
@@ -206,7 +201,7 @@ cudaError_t launch_kv_amax(const uint16_t* x, int64_t rows, int64_t cols, int64_
                            int32_t* flag, cudaStream_t stream) {
     if (rows == 0 || cols == 0) return cudaSuccess;
     const int vec = (cols % 8 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0) ? 1 : 0;
-    kv_amax_kernel<<<kv_grid(vec ? rows * (cols / 8) / 4 : rows * cols), 256, 0, stream>>>(x, rows, cols, ld, vec,
+    kv_amax_kernel<<<kv_grid(rows * 32), 256, 0, stream>>>(x, rows, cols, ld, vec,
                                                                                      amax_bits, flag);
     return cudaGetLastError();
 }
@@ -225,7 +220,7 @@ cudaError_t launch_kv_append(const uint16_t* x, int64_t rows, int64_t cols, int6
                      (reinterpret_cast<uintptr_t>(cache) & 7u) == 0)
                         ? 1
                         : 0;
-    kv_append_kernel<<<kv_grid(vec ? rows * (cols / 8) / 4 : rows * cols), 256, 0, stream>>>(
+    kv_append_kernel<<<kv_grid(rows * 32), 256, 0, stream>>>(
         x, rows, cols, ld_x, scale, slots, cache, ld_c, num_slots, vec, saturated, flag);
     return cudaGetLastError();
 }

@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Launch one kernel shape a few times (target for `ncu -k regex:... -s W -c N`).
-usage: one_gemm.py gemm M N K | wq N K | aq M K | rms M K | silu M I | grouped T name [skew]"""
+usage: one_gemm.py gemm M N K | wq N K | aq M K | rms M K | silu M I | kv T cols | grouped T name [skew]"""
 import os
 import sys
 
@@ -45,6 +45,14 @@ elif what == "silu":
     x = torch.randn((m, 2 * i), generator=g, device=dev).to(torch.bfloat16)
     for _ in range(reps):
         fp8q.silu_mul_quantize_act_per_token_group(x)
+elif what == "kv":
+    t, cols = map(int, sys.argv[2:4])
+    x = torch.randn((t, cols), generator=g, device=dev).to(torch.bfloat16)
+    amax = torch.zeros(1, dtype=torch.int32, device=dev)
+    cache = torch.empty((t, cols), dtype=torch.uint8, device=dev)
+    for _ in range(reps):
+        fp8q.kv_amax_update(x, amax)
+        fp8q.kv_quantize_append(x, fp8q.kv_scale_from_amax(amax), cache)
 elif what == "grouped":
     T = int(sys.argv[2])
     E, n, k = synth.QWEN3_30B_EXPERTS[sys.argv[3]]
