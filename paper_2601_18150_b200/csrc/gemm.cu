@@ -941,14 +941,18 @@ size_t split_ws_bytes(int64_t m, int64_t n, int sp) {
 }
 
 // Kernel choice (see launch_cfg): env FP8Q_GEMM_KIND = 128 | 256 | 1128 | 1256 overrides (dev only).
-// Default: the CTA-pair kernel, except for M < 256 where one CTA per 128 x 256 tile wastes less.
+// Default: the CTA-pair kernel for dense M >= 256, the one-CTA 128 x 256 kernel otherwise.
 int choose_kind(const GemmArgs& a) {
     static int forced = [] {
         const char* e = std::getenv("FP8Q_GEMM_KIND");
         return e ? std::atoi(e) : 0;
     }();
     if (forced == 128 || forced == 256 || forced == 1128 || forced == 1256) return forced;
-    if (a.offsets == nullptr && a.m < 2 * BM) return 256;
+    // Measured (tools/kernel_bench.py --moe, Qwen3-30B-A3B experts): the grouped GEMM's short
+    // per-expert k-loops (fc2: 6 k-blocks) and ragged segments favour the one-CTA 128 x 256
+    // tile (+5 % at T = 8192, +34-41 % at T = 1024) over the CTA pair.
+    if (a.offsets != nullptr) return 256;
+    if (a.m < 2 * BM) return 256;
     return 1256;
 }
 
