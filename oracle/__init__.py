@@ -68,6 +68,12 @@ def _load():
             lib.oracle_kv_amax.restype = ctypes.c_int
             lib.oracle_kv_quantize_append.argtypes = [P, I64, I64, I64, ctypes.c_float, P, P, I64]
             lib.oracle_kv_quantize_append.restype = ctypes.c_int64
+            lib.oracle_mx_exponent.argtypes = [ctypes.c_float]
+            lib.oracle_mx_exponent.restype = ctypes.c_int
+            lib.oracle_mx_quantize.argtypes = [P, I64, I64, I64, P, P]
+            lib.oracle_mx_quantize.restype = ctypes.c_int
+            lib.oracle_mx_gemm_rows.argtypes = [P, P, P, P, I64, I64, P, I64, P]
+            lib.oracle_mx_gemm_rows.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -278,3 +284,37 @@ def kv_quantize_append(x_bits: np.ndarray, scale: float, cache: np.ndarray, slot
     return int(_load().oracle_kv_quantize_append(_ptr(x), rows, cols, cols, float(np.float32(scale)),
                                                  _ptr(sl) if sl is not None else None, _ptr(cache),
                                                  cache.shape[1]))
+
+
+# ---------------------------------------------------------------- NEXT-4 MXFP8 variant
+def mx_exponent(amax: float) -> int:
+    """X2: the smallest e (>= -127) with 448 * 2^e >= amax; amax == 0 -> 0."""
+    return int(_load().oracle_mx_exponent(float(np.float32(amax))))
+
+
+def mx_quantize(x_bits: np.ndarray):
+    """X1-X3 on a BF16 [rows, cols] matrix: codes u8 [rows, cols] and E8M0 scale bytes
+    [rows, ceil(cols/32)] (logical layout)."""
+    x = _as_bf16_bits(x_bits)
+    rows, cols = x.shape
+    codes = np.empty((rows, cols), np.uint8)
+    sf = np.empty((rows, (cols + 31) // 32), np.uint8)
+    if _load().oracle_mx_quantize(_ptr(x), rows, cols, cols, _ptr(codes), _ptr(sf)) != 0:
+        raise OracleError("non-finite input")
+    return codes, sf
+
+
+def mx_gemm_rows(a, sfa, b, sfb, rows=None) -> np.ndarray:
+    """fp64 Y[m, n] = sum_k dec(a) 2^(sfa-127) dec(b) 2^(sfb-127) for the listed rows."""
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    sfa = np.ascontiguousarray(sfa, np.uint8)
+    sfb = np.ascontiguousarray(sfb, np.uint8)
+    m, k = a.shape
+    n = b.shape[0]
+    if b.shape[1] != k or sfa.shape != (m, (k + 31) // 32) or sfb.shape != (n, (k + 31) // 32):
+        raise OracleError("shape mismatch")
+    rows = np.arange(m, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    out = np.empty((rows.size, n), np.float64)
+    _load().oracle_mx_gemm_rows(_ptr(a), _ptr(sfa), _ptr(b), _ptr(sfb), n, k, _ptr(rows), rows.size, _ptr(out))
+    return out

@@ -416,3 +416,66 @@ int64_t oracle_kv_quantize_append(const uint16_t* x, int64_t rows, int64_t cols,
     }
     return saturated;
 }
+
+/* ================================================================== NEXT-4: MXFP8 variant
+ * SURVEY §8(f) NEXT-4 ("Blackwell ... FP8"): power-of-two (UE8M0) scales on
+ * 1x32 blocks along K for both operands, so the tensor core applies them inside the MMA
+ * (tcgen05 kind::mxf8f6f4.block_scale) and no per-k-block promotion is needed.  A DIFFERENT
+ * quantizer from the paper's amax/448 (readings X1-X3):
+ *   X1  block: 32 consecutive elements of a row along K (tokens for activations, output rows
+ *       for weights); ragged tail blocks use the in-bounds elements.
+ *   X2  scale: the smallest power of two s = 2^e with 448 s >= amax (no element saturates),
+ *       e clamped to >= -127 (the E8M0 range; codes of such tiny blocks are 0 anyway);
+ *       amax == 0 -> e = 0.  Stored as the E8M0 byte e + 127.
+ *   X3  code: O2(x / s) -- the division by a power of two is exact (a quotient that would be
+ *       an fp32 subnormal is < 2^-126, far below the E4M3 rounding point 2^-10).
+ */
+int oracle_mx_exponent(float amax) {
+    if (amax == 0.0f) return 0;
+    int e = -127;
+    while (448.0 * ldexp(1.0, e) < (double)amax) ++e; /* smallest e with 448 2^e >= amax */
+    return e;
+}
+
+/* rows x cols BF16 (row stride ld) -> codes [rows][cols], scale bytes [rows][ceil(cols/32)] */
+int oracle_mx_quantize(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld, uint8_t* codes,
+                       uint8_t* sf) {
+    int64_t nb = (cols + 31) / 32;
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t b = 0; b < nb; ++b) {
+            int64_t c0 = b * 32, c1 = c0 + 32 < cols ? c0 + 32 : cols;
+            float amax = 0.0f;
+            for (int64_t c = c0; c < c1; ++c) {
+                float v = fabsf(oracle_bf16_to_float(x[r * ld + c]));
+                if (!isfinite(v)) return ORACLE_ENONFINITE;
+                if (v > amax) amax = v;
+            }
+            int e = oracle_mx_exponent(amax);
+            sf[r * nb + b] = (uint8_t)(e + 127);
+            for (int64_t c = c0; c < c1; ++c) {
+                double q = (double)oracle_bf16_to_float(x[r * ld + c]) / ldexp(1.0, e); /* exact */
+                codes[r * cols + c] = oracle_e4m3_encode((float)q);
+            }
+        }
+    return ORACLE_OK;
+}
+
+/* fp64 reference of the MXFP8 GEMM for the listed rows:
+ *   Y[m,n] = sum_k dec(a[m,k]) 2^(sfa[m,k/32]-127) dec(b[n,k]) 2^(sfb[n,k/32]-127)          */
+int oracle_mx_gemm_rows(const uint8_t* a, const uint8_t* sfa, const uint8_t* b, const uint8_t* sfb,
+                        int64_t n, int64_t k, const int64_t* rows, int64_t nrows, double* out) {
+    int64_t nb = (k + 31) / 32;
+    for (int64_t i = 0; i < nrows; ++i) {
+        int64_t m = rows[i];
+        for (int64_t j = 0; j < n; ++j) {
+            double acc = 0.0;
+            for (int64_t kk = 0; kk < k; ++kk) {
+                double av = oracle_e4m3_decode(a[m * k + kk]) * ldexp(1.0, (int)sfa[m * nb + kk / 32] - 127);
+                double bv = oracle_e4m3_decode(b[j * k + kk]) * ldexp(1.0, (int)sfb[j * nb + kk / 32] - 127);
+                acc += av * bv;
+            }
+            out[i * n + j] = acc;
+        }
+    }
+    return ORACLE_OK;
+}
