@@ -242,6 +242,41 @@ fp8q_status kv_quantize_append(const void* x_bf16, int64_t rows, int64_t cols, i
                                const int32_t* slots, uint8_t* cache, int64_t ld_cache, int64_t num_slots,
                                uint32_t* saturated, int32_t* flag, void* stream);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT-4: MXFP8 variant (PAPER.md:235 names Blackwell FP8 support).  NOT
+ * the paper's quantizer: power-of-two E8M0 scales on 1x32 blocks along K, so the tcgen05
+ * block-scaled MMA applies them in hardware (readings X1-X3):
+ *   e = the smallest integer >= -127 with 448 * 2^e >= amax(block) (amax == 0 -> 0),
+ *   code = E4M3_RNE(x / 2^e) (exact division: no element ever saturates), scale byte = e + 127.
+ * Scale layout ("native"): byte (row r, 32-K sub-block j) at
+ *   ((r / 128) * (k / 128) + j / 4) * 512 + (r % 128) * 4 + j % 4,
+ * i.e. one contiguous 512-byte chunk per (128-row block, 128-deep k-block);
+ * mx_scale_bytes(rows, k) = ceil(rows / 128) * (k / 128) * 512.
+ * ------------------------------------------------------------------------------------------ */
+size_t mx_scale_bytes(int64_t rows, int64_t k); /* 0 for invalid sizes */
+
+/*
+ * mx_quantize -- BF16 [rows, k] (row stride ld_x) -> codes [rows, k] (row stride ld_q) and
+ *   native scale bytes (mx_scale_bytes(rows, k) bytes, caller-allocated).  Works for either
+ *   operand (activations: rows = tokens; weights: rows = output features).
+ *   Requirements: k % 128 == 0 (ESHAPE); x 16-byte aligned, ld_x % 8 == 0, codes 8-byte
+ *   aligned, ld_q % 8 == 0 (EALIGN).  nonfinite_flag as quantize_weight_blockwise.
+ */
+fp8q_status mx_quantize(const void* x_bf16, int64_t rows, int64_t k, int64_t ld_x, uint8_t* codes, int64_t ld_q,
+                        uint8_t* scales, int32_t* nonfinite_flag, void* stream);
+
+/*
+ * fp8_mx_gemm -- D[m,n] = sum_k dec(a[m,k]) 2^(sa[m,k/32]-127) dec(b[n,k]) 2^(sb[n,k/32]-127)
+ *   on the tensor cores (kind::mxf8f6f4.block_scale, fp32 accumulation in TMEM over all of K).
+ *   a [m, k], b [n, k] E4M3 codes (K-major), a_scales / b_scales native E8M0 bytes from
+ *   mx_quantize, d [m, n] BF16 or F32 (row stride ld_d elements).
+ *   Requirements: k % 128 == 0, k > 0, n % 256 == 0 (ESHAPE / EUNSUPPORTED); a, b, scales,
+ *   d 16-byte aligned, ld_a % 16 == 0, ld_b % 16 == 0, ld_d * sizeof(out) % 16 == 0 (EALIGN).
+ */
+fp8q_status fp8_mx_gemm(const uint8_t* a, int64_t ld_a, const uint8_t* a_scales, const uint8_t* b, int64_t ld_b,
+                        const uint8_t* b_scales, void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
+                        int64_t k, void* stream);
+
 /*
  * fp8q_kernel_launches -- number of kernels this library has launched in this process
  * (monotone counter; used by bench.py to report `gpu_launches`).

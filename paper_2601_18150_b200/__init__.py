@@ -9,7 +9,10 @@ from .fp8q import (  # noqa: F401
     act_scales_ld,
     fp8_block_gemm,
     fp8_block_gemm_grouped,
+    fp8_mx_gemm,
     kernel_launches,
+    mx_quantize,
+    mx_scales_logical,
     kv_amax_update,
     kv_quantize_append,
     kv_scale_from_amax,

@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfp8q.so")
-SOURCES = ["capi.cu", "quant.cu", "gemm.cu", "gemm_skinny.cu", "producers.cu", "kv.cu"]
+SOURCES = ["capi.cu", "quant.cu", "gemm.cu", "gemm_skinny.cu", "producers.cu", "kv.cu", "mx.cu"]
 HEADERS = ["ptx.cuh", "quant_kernels.h", "scale_tables.cuh", "packed.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [

@@ -227,6 +227,48 @@ fp8q_status kv_quantize_append(const void* x_bf16, int64_t rows, int64_t cols, i
     return from_cuda(e);
 }
 
+size_t mx_scale_bytes(int64_t rows, int64_t k) {
+    if (rows <= 0 || k <= 0 || k % 128 != 0) return 0;
+    return fp8q::mx_sf_bytes(rows, k);
+}
+
+fp8q_status mx_quantize(const void* x_bf16, int64_t rows, int64_t k, int64_t ld_x, uint8_t* codes, int64_t ld_q,
+                        uint8_t* scales, int32_t* nonfinite_flag, void* stream) {
+    if (rows < 0 || k < 0 || ld_x < k || ld_q < k) return FP8Q_EINVAL;
+    if (k % 128 != 0) return FP8Q_ESHAPE;
+    if (rows == 0 || k == 0) return FP8Q_OK;
+    if (x_bf16 == nullptr || codes == nullptr || scales == nullptr) return FP8Q_EINVAL;
+    if (!aligned(x_bf16, 16) || ld_x % 8 != 0 || !aligned(codes, 8) || ld_q % 8 != 0 || !aligned(nonfinite_flag, 4))
+        return FP8Q_EALIGN;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_mx_quantize(static_cast<const uint16_t*>(x_bf16), rows, k, ld_x, codes, ld_q, scales,
+                                             nonfinite_flag, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
+fp8q_status fp8_mx_gemm(const uint8_t* a, int64_t ld_a, const uint8_t* a_scales, const uint8_t* b, int64_t ld_b,
+                        const uint8_t* b_scales, void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
+                        int64_t k, void* stream) {
+    if (m < 0 || n < 0 || k < 0 || ld_a < k || ld_b < k || ld_d < n) return FP8Q_EINVAL;
+    if (d_dtype != FP8Q_OUT_BF16 && d_dtype != FP8Q_OUT_F32) return FP8Q_EINVAL;
+    if (k % 128 != 0 || n % 256 != 0) return FP8Q_ESHAPE;
+    if (m == 0 || n == 0) return FP8Q_OK;
+    if (k == 0) return FP8Q_EUNSUPPORTED;
+    if (a == nullptr || b == nullptr || a_scales == nullptr || b_scales == nullptr || d == nullptr) return FP8Q_EINVAL;
+    const int esz = d_dtype == FP8Q_OUT_F32 ? 4 : 2;
+    if (!aligned(a, 16) || !aligned(b, 16) || ld_a % 16 != 0 || ld_b % 16 != 0 || !aligned(a_scales, 16) ||
+        !aligned(b_scales, 16) || !aligned(d, 16) || (ld_d * esz) % 16 != 0)
+        return FP8Q_EALIGN;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_fp8_mx_gemm(a, ld_a, a_scales, b, ld_b, b_scales, d, ld_d, d_dtype == FP8Q_OUT_F32, m,
+                                             n, k, fp8q::tensor_map_encode_fn(), static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
 size_t fp8_block_gemm_workspace_size(int64_t m, int64_t n, int64_t k) {
     return fp8q::gemm_workspace_bytes(m, n, k, false);
 }

@@ -79,6 +79,15 @@ cudaError_t launch_kv_append(const uint16_t* x, int64_t rows, int64_t cols, int6
                              const int32_t* slots, uint8_t* cache, int64_t ld_c, int64_t num_slots,
                              uint32_t* saturated, int32_t* flag, cudaStream_t stream);
 
+// NEXT-4 MXFP8 variant (mx.cu).
+size_t mx_sf_bytes(int64_t rows, int64_t k);
+cudaError_t launch_mx_quantize(const uint16_t* x, int64_t rows, int64_t k, int64_t ld_x, uint8_t* q, int64_t ld_q,
+                               uint8_t* sf, int32_t* flag, cudaStream_t stream);
+cudaError_t launch_fp8_mx_gemm(const uint8_t* a, int64_t ld_a, const uint8_t* sfa, const uint8_t* b, int64_t ld_b,
+                               const uint8_t* sfb, void* d, int64_t ld_d, bool out_f32, int64_t m, int64_t n,
+                               int64_t k, void* encode_fn, cudaStream_t stream);
+void* tensor_map_encode_fn();
+
 // Dev-only: record a pipeline timeline of CTA 0 into dev_ptr (96 k-blocks x 12 uint32 clocks).
 void set_gemm_trace(uint32_t* dev_ptr);
 uint32_t* get_gemm_trace();

@@ -80,6 +80,12 @@ def load_library() -> ctypes.CDLL:
         lib.kv_scale_from_amax.restype = ctypes.c_int
         lib.kv_quantize_append.argtypes = [P, I64, I64, I64, P, P, P, I64, I64, P, P, P]
         lib.kv_quantize_append.restype = ctypes.c_int
+        lib.mx_scale_bytes.argtypes = [I64, I64]
+        lib.mx_scale_bytes.restype = ctypes.c_size_t
+        lib.mx_quantize.argtypes = [P, I64, I64, I64, P, I64, P, P, P]
+        lib.mx_quantize.restype = ctypes.c_int
+        lib.fp8_mx_gemm.argtypes = [P, I64, P, P, I64, P, P, I64, ctypes.c_int, I64, I64, I64, P]
+        lib.fp8_mx_gemm.restype = ctypes.c_int
         _lib = lib
         return lib
 
@@ -376,3 +382,47 @@ def kv_quantize_append(x: torch.Tensor, scale: torch.Tensor, cache: torch.Tensor
         _opt_ptr(saturated, "saturated", torch.int32), _opt_ptr(flag, "flag", torch.int32), _stream(stream)),
         "kv_quantize_append")
     return cache
+
+
+# ------------------------------------------------------------------ NEXT-4 MXFP8 variant
+def mx_quantize(x: torch.Tensor, codes: torch.Tensor | None = None, scales: torch.Tensor | None = None,
+                nonfinite_flag: torch.Tensor | None = None, stream=None):
+    """MXFP8: E4M3 codes [rows, k] + native E8M0 scale bytes (mx_scale_bytes(rows, k))."""
+    _cuda2d(x, "x", torch.bfloat16)
+    rows, k = x.shape
+    lib = load_library()
+    if codes is None:
+        codes = torch.empty((rows, k), dtype=torch.uint8, device=x.device)
+    if scales is None:
+        scales = torch.empty(max(1, int(lib.mx_scale_bytes(rows, k))), dtype=torch.uint8, device=x.device)
+    _check(lib.mx_quantize(x.data_ptr(), rows, k, _ld(x), codes.data_ptr(), _ld(codes), scales.data_ptr(),
+                           _opt_ptr(nonfinite_flag, "nonfinite_flag", torch.int32), _stream(stream)), "mx_quantize")
+    return codes, scales
+
+
+def fp8_mx_gemm(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_scales: torch.Tensor,
+                out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None, stream=None):
+    """MXFP8 linear Y = X W^T with the block-scaled tcgen05 MMA (scales from mx_quantize)."""
+    _cuda2d(a, "a", torch.uint8)
+    _cuda2d(b, "b", torch.uint8)
+    m, k = a.shape
+    n = b.shape[0]
+    if b.shape[1] != k:
+        raise Fp8qError("fp8_mx_gemm: inner dimensions differ")
+    out = _out(out, m, n, out_dtype, a.device)
+    _check(load_library().fp8_mx_gemm(a.data_ptr(), _ld(a), a_scales.data_ptr(), b.data_ptr(), _ld(b),
+                                      b_scales.data_ptr(), out.data_ptr(), _ld(out),
+                                      FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16, m, n, k,
+                                      _stream(stream)), "fp8_mx_gemm")
+    return out
+
+
+def mx_scales_logical(native, rows: int, k: int):
+    """Native scale bytes -> the logical [rows, k/32] array (for tests and inspection)."""
+    import numpy as np
+    nat = np.asarray(native.cpu().numpy() if hasattr(native, "cpu") else native, dtype=np.uint8)
+    kb = k // 128
+    blocks = (rows + 127) // 128
+    t = nat[: blocks * kb * 512].reshape(blocks, kb, 128, 4)      # [rb][kb][r%128][j%4]
+    t = t.transpose(0, 2, 1, 3).reshape(blocks * 128, kb * 4)     # [r][j]
+    return t[:rows]

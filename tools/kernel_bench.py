@@ -135,6 +135,24 @@ def main():
                     rec.update({"graph_ms": round(tg, 4), "graph_GBps": round(by / (tg * 1e-3) / 1e9, 1),
                                 "graph_frac_hbm": round(by / (tg * 1e-3) / 1e9 / HBM, 4)})
                 print(json.dumps(rec))
+    if args.what in ("all", "mx"):
+        # NEXT-4: MXFP8 quantizer (2 + 1 + 1/32 B per element) and block-scaled GEMM, Qwen3-8B M = 8192
+        M = 8192
+        for name, (n, k) in synth.QWEN3_8B_LINEARS.items():
+            w = (torch.randn((n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+            x = torch.randn((M, k), generator=g, device=dev).to(torch.bfloat16)
+            wq, ws = fp8q.mx_quantize(w)
+            xq, xs = fp8q.mx_quantize(x)
+            t, lo, hi = timeit(lambda: fp8q.mx_quantize(x, xq, xs), args.iters, flush)
+            by = M * k * (3 + 1 / 32)
+            print(json.dumps({"kernel": "mx_quantize", "shape": [M, k], "ms": round(t, 4),
+                              "GBps": round(by / (t * 1e-3) / 1e9, 1), "frac_hbm": round(by / (t * 1e-3) / 1e9 / HBM, 4)}))
+            y = torch.empty((M, n), dtype=torch.bfloat16, device=dev)
+            t, lo, hi = timeit(lambda: fp8q.fp8_mx_gemm(xq, xs, wq, ws, out=y), args.iters, flush)
+            tf = 2 * M * n * k / (t * 1e-3) / 1e12
+            print(json.dumps({"kernel": "fp8_mx_gemm", "name": name, "shape": [M, n, k], "ms": round(t, 4),
+                              "p10": round(lo, 4), "p90": round(hi, 4), "TFLOPs": round(tf, 1),
+                              "frac_fp8": round(tf / FP8, 4)}))
     if args.what in ("all", "kv"):
         # NEXT-3: calibration amax (2 B/elem) and append (3 B/elem) on Qwen3-8B K (8 heads x 128)
         cols = 8 * 128
