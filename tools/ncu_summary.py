@@ -25,6 +25,8 @@ KEYS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("smsp__mem_tensor_reads_op_ldt.sum.pct_of_peak_sustained_elapsed", "TMEM ld (LDTM) %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem (LSU) wavefronts %"),
+    ("sm__memory_throughput.avg.pct_of_peak_sustained_elapsed", "SM memory throughput %"),
 ]
 
 

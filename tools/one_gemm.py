@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Launch one kernel shape a few times (target for `ncu -k regex:... -s W -c N`).
-usage: one_gemm.py gemm M N K | wq N K | aq M K | rms M K | silu M I | kv T cols | grouped T name [skew]"""
+usage: one_gemm.py gemm M N K | wq N K | aq M K | rms M K | silu M I | kv T cols | mxgemm M N K | grouped T name [skew]"""
 import os
 import sys
 
@@ -45,6 +45,15 @@ elif what == "silu":
     x = torch.randn((m, 2 * i), generator=g, device=dev).to(torch.bfloat16)
     for _ in range(reps):
         fp8q.silu_mul_quantize_act_per_token_group(x)
+elif what == "mxgemm":
+    m, n, k = map(int, sys.argv[2:5])
+    w = (torch.randn((n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    x = torch.randn((m, k), generator=g, device=dev).to(torch.bfloat16)
+    wq, ws = fp8q.mx_quantize(w)
+    xq, xs = fp8q.mx_quantize(x)
+    y = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
+    for _ in range(reps):
+        fp8q.fp8_mx_gemm(xq, xs, wq, ws, out=y)
 elif what == "kv":
     t, cols = map(int, sys.argv[2:4])
     x = torch.randn((t, cols), generator=g, device=dev).to(torch.bfloat16)
