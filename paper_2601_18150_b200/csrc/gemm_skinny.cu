@@ -112,6 +112,8 @@ __device__ __forceinline__ void sk_trace_cta(const SkParams& p, int which) {
     }
 }
 
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Walks this CTA's segments: (tile, kb0, kb1) = k-blocks [kb0, kb1) of weight tile `tile`.
 struct SegIter {
     int64_t x, end;  // stream-K: position in [0, T) and this CTA's range end
@@ -241,6 +243,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     if (threadIdx.x == 0) sk_trace(p, 0, 5);
+    // let the next kernel in the stream (launched with programmatic stream serialization)
+    // start its prologue and weight prefetch on SMs this grid vacates
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp < SK_EPI_WARP0) regs_dec<SK_REGS_CTRL>();
 
     if (warp == 0) {
@@ -249,19 +254,39 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             tma_prefetch_desc(&tmW);
             tma_prefetch_desc(&tmX);
             tma_prefetch_desc(&tmS);
+            // Programmatic dependent launch: the weights (and their scales) are never written by
+            // the kernel this one may overlap (only this kernel triggers early, see below), so
+            // the first ring fill of weight tiles is issued before waiting for the previous
+            // grid; the activations and their scales (its possible outputs) only after.
             uint32_t it = 0;
             SegIter seg;
             seg.init(p);
             int tile, kb0, kb1;
+            {
+                SegIter pre = seg;
+                int pt, pk0, pk1;
+                uint32_t n = 0;
+                while (n < STAGES && pre.next(p, pt, pk0, pk1))
+                    for (int kb = pk0; kb < pk1 && n < STAGES; ++kb, ++n) {
+                        mbar_arrive_expect_tx(&full[n], C::STAGE_BYTES + C::SA_BYTES);
+                        tma_load_2d(smW + n * C::W_TILE, &tmW, &full[n], kb * SK_BK, pt * SK_BN);
+                    }
+            }
+            grid_dependency_wait();
             while (seg.next(p, tile, kb0, kb1)) {
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
-                    mbar_wait(&empty[stage], ph ^ 1u);
-                    mbar_wait(&sempty[stage], ph ^ 1u);
+                    const bool prefetched = it < STAGES;  // W already in flight, expect_tx armed
+                    if (!prefetched) {
+                        mbar_wait(&empty[stage], ph ^ 1u);
+                        mbar_wait(&sempty[stage], ph ^ 1u);
+                    }
                     sk_trace(p, it, 0);
-                    mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES + C::SA_BYTES);
-                    tma_load_2d(smW + stage * C::W_TILE, &tmW, &full[stage], kb * SK_BK, tile * SK_BN);
+                    if (!prefetched) {
+                        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES + C::SA_BYTES);
+                        tma_load_2d(smW + stage * C::W_TILE, &tmW, &full[stage], kb * SK_BK, tile * SK_BN);
+                    }
                     tma_load_2d(smX + stage * C::X_TILE, &tmX, &full[stage], kb * SK_BK, 0);
                     tma_load_2d(smS + stage * SA_STRIDE, &tmS, &full[stage], 0, kb);
                 }
@@ -300,6 +325,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     } else if (warp >= SK_EPI_WARP0) {
         // ---------------------------------------------------------------- promotion warps
         regs_inc<SK_REGS_EPI>();
+        grid_dependency_wait();  // before any global write (D, workspace): the previous grid is done
         const int qd = warp & 3;                       // TMEM lane quarter of this warp
         const int h = (warp - SK_EPI_WARP0) >> 2;      // token-column half
         const int r_in = qd * 32 + lane;               // weight row within the tile
@@ -541,8 +567,17 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
         p.ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + SK_COUNTER_BYTES);
         grid = static_cast<unsigned>(sk_grid(p.tiles, p.num_kb, sms));
     }
-    fp8_gemm_skinny_kernel<MT><<<grid, SK_THREADS, SkCfg<MT>::SMEM_BYTES, stream>>>(tmW, tmX, tmS, p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(SK_THREADS);
+    cfg.dynamicSmemBytes = SkCfg<MT>::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT>, tmW, tmX, tmS, p);
 }
 
 }  // namespace
