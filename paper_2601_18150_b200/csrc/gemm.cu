@@ -92,6 +92,7 @@ struct KParams {
     int num_n_tiles;
     const int32_t* offsets;  // nullptr: one group of m rows
     int splits;              // split-K slices per tile (one-CTA kernel, dense, small M); 1 = off
+    int raster;              // m-tiles per raster band (TileCursor)
     float* ws;               // split-K partials [tile][split][128][BN] fp32
     int32_t* counters;       // split-K arrival counters [tile], zero between launches
     uint32_t* trace;         // dev-only timeline (fp8q_debug_set_trace), nullptr in production
@@ -110,7 +111,7 @@ __device__ __forceinline__ void trace_ev(const KParams& p, uint32_t it, int ev) 
 
 // Walks the (group, m-tile, n-tile) sequence; t must increase between calls.  TM = rows per
 // tile (128 for one CTA, 256 for a CTA pair), GM = m-tiles per raster band.
-template <int TM, int GM>
+template <int TM, int GM_UNUSED>
 struct TileCursor {
     // 32-bit tile arithmetic on purpose: 64-bit division is a ~100-instruction software
     // routine, and this runs between tiles on the promotion warps' critical path.
@@ -145,11 +146,12 @@ struct TileCursor {
         // Grouped raster: bands of GM m-tiles; inside a band m is fastest, so the ~148
         // concurrent tiles cover a compact RASTER_GM x ~9 block of the output and both the A
         // band and the B tiles they touch stay L2-resident (K = 12288 would otherwise re-read A).
+        const unsigned GM = static_cast<unsigned>(p.raster);
         const unsigned l = static_cast<unsigned>(t - base);
-        const unsigned span = static_cast<unsigned>(GM * p.num_n_tiles);
+        const unsigned span = GM * static_cast<unsigned>(p.num_n_tiles);
         const unsigned band = l / span;
         const unsigned r = l - band * span;
-        const unsigned gm = min(static_cast<unsigned>(GM), static_cast<unsigned>(mtiles) - band * GM);
+        const unsigned gm = min(GM, static_cast<unsigned>(mtiles) - band * GM);
         const unsigned q = r / gm;
         mt = static_cast<int>(band * GM + (r - q * gm));
         nt = static_cast<int>(q);
@@ -1026,6 +1028,20 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
     p.splits = 1;
     p.ws = nullptr;
     p.counters = nullptr;
+    {
+        // raster band: as many m-tiles as keep the band's A panel (rows x K bytes) within
+        // ~32 MB of L2, so B streams from HBM once per band (FP8Q_GEMM_RASTER overrides, dev)
+        static const int forced_raster = [] {
+            const char* e = std::getenv("FP8Q_GEMM_RASTER");
+            return e ? std::atoi(e) : 0;
+        }();
+        const int64_t tile_rows = kPair ? 2 * BM : BM;
+        int64_t r = (32LL << 20) / (tile_rows * (a.k > 0 ? a.k : 1));
+        r = r < 4 ? 4 : (r > 64 ? 64 : r);
+        // measured (FP8Q_GEMM_RASTER sweep, pair kernel): gate_up (K = 4096) +1.5 % at 32
+        // m-tiles per band vs 8; down (K = 12288) best at 8-16; qkv / o insensitive
+        p.raster = forced_raster > 0 ? forced_raster : (kPair ? static_cast<int>(r) : RASTER_GM);
+    }
     if (!kPair && KIND == 256 && a.offsets == nullptr) {
         const int sp = plan_splits(a.m, a.n, a.k, sms);
         const size_t need = split_ws_bytes(a.m, a.n, sp);
