@@ -468,9 +468,19 @@ def run_sync(args):
     torch.cuda.set_device(device)
     peaks = load_peaks()
     from paper_2601_18150_b200 import fp8q
-    from paper_2601_18150_b200.sync import WeightSyncEngine
+    from paper_2601_18150_b200.sync import WeightSyncEngine, symmetric_peer_buffers
     specs = model_specs(args.workload)
-    eng = WeightSyncEngine(specs, device)
+    mode = "quantize shard + grouped NCCL all-gather"
+    peers = None
+    if args.fanout and world > 1:
+        # NEXT-1: the quantizer stores into every rank's symmetric-memory engine buffer (P2P
+        # over NVLink), no gather pass; falls back to the gather mode if unavailable
+        try:
+            peers = symmetric_peer_buffers(specs, device)
+            mode = "fan-out quantizer (P2P stores into every rank's symmetric-memory buffer)"
+        except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+            mode = f"gather (fan-out unavailable: {type(exc).__name__}: {exc})"[:200]
+    eng = WeightSyncEngine(specs, device, peers=peers)
     gen = torch.Generator(device=device)
     shards = {}
     local_elems = 0
@@ -525,7 +535,7 @@ def run_sync(args):
         "vs_baseline": None, "dtype": "bf16 -> fp8_e4m3", "data": "synthetic (device-generated seeded BF16)",
         "config": {"workload": f"{args.workload}_whole_model_weight_sync", "tensors": len(specs),
                    "quantized_params": total_elems, "fp8_bytes": fp8_bytes,
-                   "parallelism": f"requant sharded over {world} ranks (128-row blocks / experts) + grouped NCCL all-gather of FP8 codes and scales",
+                   "parallelism": f"requant sharded over {world} ranks (128-row blocks / experts); exchange: {mode}",
                    "l2": "inputs larger than L2 (whole model)"},
         "breakdown": {"floor_quantize_ms": round(floor_q, 3), "floor_allgather_ms_770GBps": round(floor_g, 3),
                       "floor_ms": round(max(floor_q, floor_g), 3),
@@ -553,6 +563,7 @@ def main(argv=None):
     ap.add_argument("--workload", choices=["layer8b", "sync8b", "sync30b"], default="layer8b")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fanout", action="store_true", help="sync workloads: NEXT-1 fan-out quantizer (N > 1)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -104,6 +104,25 @@ fp8q_status quantize_weight_blockwise_batched(const fp8q_weight_tensor* tensors,
                                               int32_t* nonfinite_flag, void* stream);
 
 /*
+ * quantize_weight_blockwise_fanout -- SURVEY §8(f) NEXT-1: the per-step requant of a rank's
+ *   shard written straight into EVERY rank's engine buffer, so no separate all-gather pass
+ *   re-reads the codes ("retrieved ... quantized ... loaded").  Same element map
+ *   as quantize_weight_blockwise_batched; each code / scale store goes to
+ *       tensors[i].codes + codes_delta[d]   and   tensors[i].scales + scales_delta[d] (bytes)
+ *   for d in [0, num_dest): peer-mapped buffers of identical layout (e.g. torch symmetric
+ *   memory: delta = peer base - local base; include delta 0 for the local copy).  Over
+ *   NVLink/NVSwitch the stores are P2P writes issued by the quantizer itself.  The caller
+ *   orders the peers' reads after the launch (e.g. a barrier on the symmetric-memory handle).
+ *   Requirements: 1 <= num_dest <= 8 (EINVAL); codes_delta % 16 == 0, scales_delta % 4 == 0
+ *   (EALIGN); every tensor on the wide path: k % 16 == 0, w 32-byte aligned, ld_w % 16 == 0,
+ *   codes 16-byte aligned, ld_q % 16 == 0 (EUNSUPPORTED otherwise); the rest as
+ *   quantize_weight_blockwise.
+ */
+fp8q_status quantize_weight_blockwise_fanout(const fp8q_weight_tensor* tensors, int32_t count, int32_t num_dest,
+                                             const int64_t* codes_delta, const int64_t* scales_delta,
+                                             int32_t* nonfinite_flag, void* stream);
+
+/*
  * quantize_act_per_token_group -- dynamic activation quantization, PAPER.md:46,65,73;
  * granularity 1x128 (per token m, per 128-channel group g).
  *   x_bf16  [m, k] BF16, row stride ld_x.

@@ -110,6 +110,43 @@ fp8q_status quantize_weight_blockwise_batched(const fp8q_weight_tensor* tensors,
     return FP8Q_OK;
 }
 
+fp8q_status quantize_weight_blockwise_fanout(const fp8q_weight_tensor* tensors, int32_t count, int32_t num_dest,
+                                             const int64_t* codes_delta, const int64_t* scales_delta,
+                                             int32_t* nonfinite_flag, void* stream) {
+    if (count < 0 || (count > 0 && tensors == nullptr)) return FP8Q_EINVAL;
+    if (num_dest < 1 || num_dest > fp8q::kMaxFanout || codes_delta == nullptr || scales_delta == nullptr)
+        return FP8Q_EINVAL;
+    if (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)) return FP8Q_EALIGN;
+    for (int32_t d = 0; d < num_dest; ++d)
+        if (codes_delta[d] % 16 != 0 || scales_delta[d] % 4 != 0) return FP8Q_EALIGN;
+    for (int32_t i = 0; i < count; ++i) {
+        const fp8q_weight_tensor& t = tensors[i];
+        fp8q_status st = check_weight(t.w_bf16, t.n, t.k, t.ld_w, t.codes, t.ld_q, t.scales, t.ld_s);
+        if (st != FP8Q_OK) return st;
+        // the fan-out runs on the wide path only: k % 16, 32-byte-aligned w, ld_w % 16,
+        // 16-byte-aligned codes, ld_q % 16
+        if (t.k % 16 != 0 || !aligned(t.w_bf16, 32) || t.ld_w % 16 != 0 || !aligned(t.codes, 16) || t.ld_q % 16 != 0)
+            return FP8Q_EUNSUPPORTED;
+    }
+    if (count == 0) return FP8Q_OK;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    fp8q::WeightDesc d[fp8q::kMaxWeightBatch];
+    for (int32_t base = 0; base < count; base += fp8q::kMaxWeightBatch) {
+        const int32_t c = count - base < fp8q::kMaxWeightBatch ? count - base : fp8q::kMaxWeightBatch;
+        for (int32_t i = 0; i < c; ++i) {
+            const fp8q_weight_tensor& t = tensors[base + i];
+            d[i] = fp8q::WeightDesc{static_cast<const uint16_t*>(t.w_bf16), t.n, t.k, t.ld_w, t.codes, t.ld_q,
+                                    t.scales, t.ld_s};
+        }
+        cudaError_t e = fp8q::launch_weight_blockwise_batch(d, c, nonfinite_flag, static_cast<cudaStream_t>(stream),
+                                                            num_dest, codes_delta, scales_delta);
+        if (e != cudaSuccess) return FP8Q_ECUDA;
+        g_launches.fetch_add(fp8q::weight_batch_launches(d, c));
+    }
+    return FP8Q_OK;
+}
+
 fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t k, int64_t ld_x,
                                          uint8_t* codes, int64_t ld_q, float* scales, int64_t ld_s,
                                          int32_t* nonfinite_flag, void* stream) {

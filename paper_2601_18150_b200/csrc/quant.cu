@@ -255,6 +255,12 @@ struct WBatch {
     WTensor t[kMaxWeightBatch];
     int count;
     int64_t nblocks;
+    // NEXT-1 fan-out: ndest > 0 -> every code / scale store goes to pointer + dq[d] / ds[d]
+    // for each destination d (peer-mapped buffers of identical layout, e.g. symmetric
+    // memory: the quantized shard lands in every rank's engine buffer, no separate gather)
+    int ndest;
+    int64_t dq[kMaxFanout];
+    int64_t ds[kMaxFanout];
 };
 __device__ __forceinline__ void wq_load(const uint16_t* __restrict__ w, int64_t n, int64_t k,
                                         int64_t ld_w, int64_t nbk, int64_t blk, WBlockRegs& d) {
@@ -273,10 +279,19 @@ __device__ __forceinline__ void wq_load(const uint16_t* __restrict__ w, int64_t 
         }
     }
 }
+template <bool kFanout>
+__device__ __forceinline__ void wq_store(uint8_t* dst, const uint4& c, const WBatch& bt) {
+    if (kFanout) {
+        for (int dd = 0; dd < bt.ndest; ++dd) st_v4_na(dst + bt.dq[dd], c);
+    } else {
+        st_v4_na(dst, c);
+    }
+}
+template <bool kFanout>
 __device__ __forceinline__ void wq_process(const WBlockRegs& d, int64_t n, int64_t k, uint8_t* __restrict__ q,
                                            int64_t ld_q, float* __restrict__ scales, int64_t ld_s,
                                            int64_t nbk, int64_t blk, uint32_t* red,
-                                           int32_t* __restrict__ nonfinite_flag) {
+                                           int32_t* __restrict__ nonfinite_flag, const WBatch& bt) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t bi = blk / nbk, bj = blk - (blk / nbk) * nbk;
     const int64_t col = bj * 128 + (lane & 7) * 16;
@@ -292,7 +307,12 @@ __device__ __forceinline__ void wq_process(const WBlockRegs& d, int64_t n, int64
     for (int i = 1; i < 8; ++i) ab = max(ab, red[i]);
     const float s = scale_from_amax_bits(ab);
     if (threadIdx.x == 0) {
-        scales[bi * ld_s + bj] = s;
+        if (kFanout) {
+            for (int dd = 0; dd < bt.ndest; ++dd)
+                *reinterpret_cast<float*>(reinterpret_cast<char*>(scales + bi * ld_s + bj) + bt.ds[dd]) = s;
+        } else {
+            scales[bi * ld_s + bj] = s;
+        }
         if (ab >= kNonFiniteBits && nonfinite_flag != nullptr) *nonfinite_flag = 1;
     }
     const bool col_ok = col < k;
@@ -301,18 +321,19 @@ __device__ __forceinline__ void wq_process(const WBlockRegs& d, int64_t n, int64
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t row = row0 + 4 * i;
-            if (col_ok && row < n) st_v4_na(q + row * ld_q + col, encode16<true>(d.v[i], s, r));
+            if (col_ok && row < n) wq_store<kFanout>(q + row * ld_q + col, encode16<true>(d.v[i], s, r), bt);
         }
     } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t row = row0 + 4 * i;
-            if (col_ok && row < n) st_v4_na(q + row * ld_q + col, encode16<false>(d.v[i], s, 0.0f));
+            if (col_ok && row < n) wq_store<kFanout>(q + row * ld_q + col, encode16<false>(d.v[i], s, 0.0f), bt);
         }
     }
 }
 // A batch of weight tensors quantized by ONE launch (the weight sync re-quantizes every
 // linear weight of a layer at once: one launch instead of one per tensor).
+template <bool kFanout>
 __global__ void __launch_bounds__(256, 2) weight_blockwise_wide_kernel(const __grid_constant__ WBatch bt,
                                                                         int32_t* __restrict__ nonfinite_flag) {
     __shared__ uint32_t red[2][8];
@@ -329,7 +350,7 @@ __global__ void __launch_bounds__(256, 2) weight_blockwise_wide_kernel(const __g
     };
     auto process = [&](int64_t blk, const WBlockRegs& d, uint32_t* rd) {
         const WTensor& t = bt.t[tensor_of(blk)];
-        wq_process(d, t.n, t.k, t.q, t.ld_q, t.scales, t.ld_s, t.nbk, blk - t.blk0, rd, nonfinite_flag);
+        wq_process<kFanout>(d, t.n, t.k, t.q, t.ld_q, t.scales, t.ld_s, t.nbk, blk - t.blk0, rd, nonfinite_flag, bt);
     };
     int64_t blk = blockIdx.x;
     if (blk < nblocks) load(blk, a);
@@ -449,16 +470,29 @@ bool wide_ok(const WeightDesc& d) {
 }  // namespace
 
 cudaError_t launch_weight_blockwise_batch(const WeightDesc* descs, int count, int32_t* flag,
-                                          cudaStream_t stream) {
+                                          cudaStream_t stream, int ndest, const int64_t* dq, const int64_t* ds) {
     // wide path for every aligned tensor, batched kMaxWeightBatch per launch
     WBatch bt{};
     bt.count = 0;
     bt.nblocks = 0;
+    bt.ndest = ndest;
+    for (int dd = 0; dd < ndest && dd < kMaxFanout; ++dd) {
+        bt.dq[dd] = dq[dd];
+        bt.ds[dd] = ds[dd];
+    }
+    if (ndest > 0)
+        for (int i = 0; i < count; ++i)
+            if (!wide_ok(descs[i])) return cudaErrorInvalidValue;  // fan-out runs on the wide path only
     auto flush = [&]() -> cudaError_t {
         if (bt.count == 0) return cudaSuccess;
         const int64_t cap = 2LL * sm_count();
         const int64_t grid = bt.nblocks < cap ? bt.nblocks : cap;
-        if (grid > 0) weight_blockwise_wide_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(bt, flag);
+        if (grid > 0) {
+            if (bt.ndest > 0)
+                weight_blockwise_wide_kernel<true><<<static_cast<unsigned>(grid), 256, 0, stream>>>(bt, flag);
+            else
+                weight_blockwise_wide_kernel<false><<<static_cast<unsigned>(grid), 256, 0, stream>>>(bt, flag);
+        }
         bt.count = 0;
         bt.nblocks = 0;
         return cudaGetLastError();

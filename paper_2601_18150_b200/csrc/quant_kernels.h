@@ -6,6 +6,7 @@
 namespace fp8q {
 
 constexpr int kMaxWeightBatch = 16;  // tensors per batched weight-quantization launch
+constexpr int kMaxFanout = 8;        // destinations of the fan-out (NEXT-1) weight quantizer
 
 struct WeightDesc {
     const uint16_t* w;
@@ -19,7 +20,8 @@ struct WeightDesc {
 // All descs in as few launches as possible (kMaxWeightBatch wide-path tensors per launch;
 // tensors that miss the wide path's alignment get their own launch of the general kernel).
 cudaError_t launch_weight_blockwise_batch(const WeightDesc* descs, int count, int32_t* flag,
-                                          cudaStream_t stream);
+                                          cudaStream_t stream, int ndest = 0, const int64_t* dq = nullptr,
+                                          const int64_t* ds = nullptr);
 int weight_batch_launches(const WeightDesc* descs, int count);
 
 cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int64_t ld_w,

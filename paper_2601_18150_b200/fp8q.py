@@ -56,6 +56,8 @@ def load_library() -> ctypes.CDLL:
         lib.quantize_weight_blockwise.restype = ctypes.c_int
         lib.quantize_weight_blockwise_batched.argtypes = [ctypes.POINTER(WeightTensorDesc), I32, P, P]
         lib.quantize_weight_blockwise_batched.restype = ctypes.c_int
+        lib.quantize_weight_blockwise_fanout.argtypes = [ctypes.POINTER(WeightTensorDesc), I32, I32, P, P, P, P]
+        lib.quantize_weight_blockwise_fanout.restype = ctypes.c_int
         lib.quantize_act_per_token_group.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
         lib.quantize_act_per_token_group.restype = ctypes.c_int
         lib.rmsnorm_quantize_act_per_token_group.argtypes = [P, P, ctypes.c_float, I64, I64, I64, P, I64, P, I64,
@@ -166,6 +168,33 @@ def quantize_weight_blockwise_batched(items, nonfinite_flag: torch.Tensor | None
     flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
     _check(load_library().quantize_weight_blockwise_batched(arr, len(items), flag, _stream(stream)),
            "quantize_weight_blockwise_batched")
+
+
+def quantize_weight_blockwise_fanout(items, codes_delta, scales_delta, nonfinite_flag: torch.Tensor | None = None,
+                                     stream=None):
+    """NEXT-1: quantize_weight_blockwise_batched whose code / scale stores go to every
+    destination: pointer + codes_delta[d] / scales_delta[d] (bytes; peer-mapped buffers of
+    identical layout, delta 0 = the local buffer)."""
+    items = list(items)
+    arr = (WeightTensorDesc * max(1, len(items)))()
+    for i, (w, codes, scales) in enumerate(items):
+        _cuda2d(w, "w", torch.bfloat16)
+        _cuda2d(codes, "codes", torch.uint8)
+        _cuda2d(scales, "scales", torch.float32)
+        n, k = w.shape
+        if codes.shape != (n, k) or scales.shape[0] < (n + 127) // 128 or scales.shape[1] < (k + 127) // 128:
+            raise Fp8qError(f"item {i}: output shape mismatch")
+        arr[i] = WeightTensorDesc(w.data_ptr(), n, k, _ld(w), codes.data_ptr(), _ld(codes),
+                                  scales.data_ptr(), _ld(scales))
+    nd = len(codes_delta)
+    if nd != len(scales_delta):
+        raise Fp8qError("codes_delta and scales_delta must have one entry per destination")
+    cd = (ctypes.c_int64 * max(1, nd))(*[int(v) for v in codes_delta])
+    sd = (ctypes.c_int64 * max(1, nd))(*[int(v) for v in scales_delta])
+    flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
+    _check(load_library().quantize_weight_blockwise_fanout(arr, len(items), nd, ctypes.cast(cd, ctypes.c_void_p),
+                                                           ctypes.cast(sd, ctypes.c_void_p), flag, _stream(stream)),
+           "quantize_weight_blockwise_fanout")
 
 
 def act_scales_ld(m: int) -> int:

@@ -92,6 +92,65 @@ def plan_shards(spec: TensorSpec, world: int) -> List[Shard]:
 QuantizeFn = Callable[[torch.Tensor, torch.Tensor, torch.Tensor], None]
 
 
+class PeerBuffers:
+    """NEXT-1: engine buffers of identical layout on several destinations.  The
+    fan-out quantizer stores every code / scale of this rank's shard at pointer + delta[d] for
+    each destination d, so every rank's engine buffer receives the shard straight from the
+    quantizer (P2P stores over NVLink) and no all-gather pass re-reads it.
+
+    codes_flat / scales_flat are this rank's (local) flat buffers; the engine lays its
+    per-tensor views into them.  `fence()` orders the peers' later reads after the stores."""
+
+    def __init__(self, codes_flat, scales_flat, codes_delta, scales_delta, fence=None, keep=()):
+        self.codes_flat = codes_flat
+        self.scales_flat = scales_flat
+        self.codes_delta = [int(d) for d in codes_delta]
+        self.scales_delta = [int(d) for d in scales_delta]
+        self._fence = fence
+        self._keep = keep  # owners of the destination memory
+
+    def fence(self) -> None:
+        if self._fence is not None:
+            self._fence()
+
+
+def _layout(specs):
+    """Byte / element offsets of each tensor's codes and scales in the flat buffers (256-B aligned)."""
+    co, so, c_off, s_off = {}, {}, 0, 0
+    for s in specs:
+        co[s.name] = c_off
+        so[s.name] = s_off
+        c_off += -(-(s.rows * s.k) // 256) * 256
+        s_off += -(-(s.scale_rows * s.scale_cols) // 64) * 64
+    return co, so, c_off, s_off
+
+
+def local_replica_buffers(specs, device, replicas: int) -> PeerBuffers:
+    """Fan-out onto `replicas` buffers of this GPU (destination 0 is the engine's own): the
+    single-GPU stand-in for peers, used by the tests and the single-GPU bench."""
+    _, _, nc, ns = _layout(specs)
+    cs = [torch.zeros(nc, dtype=torch.uint8, device=device) for _ in range(replicas)]
+    ss = [torch.zeros(ns, dtype=torch.float32, device=device) for _ in range(replicas)]
+    return PeerBuffers(cs[0], ss[0], [c.data_ptr() - cs[0].data_ptr() for c in cs],
+                       [x.data_ptr() - ss[0].data_ptr() for x in ss], keep=(cs, ss))
+
+
+def symmetric_peer_buffers(specs, device, group=None) -> PeerBuffers:
+    """Engine buffers in torch symmetric memory: every rank's buffer is mapped into every other
+    rank's address space over NVLink, so the fan-out deltas are peer base - local base.  The
+    fence is the symmetric-memory barrier (all ranks' stores done before anyone reads)."""
+    import torch.distributed._symmetric_memory as symm_mem
+    _, _, nc, ns = _layout(specs)
+    group = group or dist.group.WORLD
+    c = symm_mem.empty(nc, dtype=torch.uint8, device=device)
+    s = symm_mem.empty(ns, dtype=torch.float32, device=device)
+    hc = symm_mem.rendezvous(c, group)
+    hs = symm_mem.rendezvous(s, group)
+    cd = [p - c.data_ptr() for p in hc.buffer_ptrs]
+    sd = [p - s.data_ptr() for p in hs.buffer_ptrs]
+    return PeerBuffers(c, s, cd, sd, fence=lambda: hc.barrier(), keep=(c, s, hc, hs))
+
+
 def _default_quantize(w: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor) -> None:
     from .fp8q import quantize_weight_blockwise
     quantize_weight_blockwise(w, codes, scales)
@@ -103,8 +162,9 @@ class WeightSyncEngine:
     rejection, post-state equals quantize(snapshot) bitwise)."""
 
     def __init__(self, specs: Sequence[TensorSpec], device, group=None,
-                 quantize_fn: Optional[QuantizeFn] = None):
+                 quantize_fn: Optional[QuantizeFn] = None, peers: Optional[PeerBuffers] = None):
         self.specs = list(specs)
+        self.peers = peers
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -113,10 +173,17 @@ class WeightSyncEngine:
         self.plans: Dict[str, List[Shard]] = {s.name: plan_shards(s, self.world) for s in self.specs}
         self.codes: Dict[str, torch.Tensor] = {}
         self.scales: Dict[str, torch.Tensor] = {}
-        for s in self.specs:
-            self.codes[s.name] = torch.empty((s.rows, s.k), dtype=torch.uint8, device=self.device)
-            self.scales[s.name] = torch.empty((s.scale_rows, s.scale_cols), dtype=torch.float32,
-                                              device=self.device)
+        if peers is not None:
+            co, so, _, _ = _layout(self.specs)
+            for s in self.specs:
+                self.codes[s.name] = peers.codes_flat[co[s.name]:co[s.name] + s.rows * s.k].view(s.rows, s.k)
+                nsc = s.scale_rows * s.scale_cols
+                self.scales[s.name] = peers.scales_flat[so[s.name]:so[s.name] + nsc].view(s.scale_rows, s.scale_cols)
+        else:
+            for s in self.specs:
+                self.codes[s.name] = torch.empty((s.rows, s.k), dtype=torch.uint8, device=self.device)
+                self.scales[s.name] = torch.empty((s.scale_rows, s.scale_cols), dtype=torch.float32,
+                                                  device=self.device)
         self.loaded_step = -1
 
     def my_shard(self, name: str) -> Shard:
@@ -179,6 +246,15 @@ class WeightSyncEngine:
         missing = [s.name for s in self.specs if s.name not in shards]
         if missing:
             raise KeyError(f"missing shards: {missing}")
+        if self.peers is not None:
+            # NEXT-1: the quantizer writes every rank's buffer itself; no gather pass
+            from .fp8q import quantize_weight_blockwise_fanout
+            for b0 in range(0, len(self.specs), bucket):
+                quantize_weight_blockwise_fanout(self._local_items(self.specs[b0:b0 + bucket], shards),
+                                                 self.peers.codes_delta, self.peers.scales_delta)
+            self.peers.fence()
+            self.loaded_step = step
+            return
         batched = self.quantize_fn is _default_quantize
         if batched:
             from .fp8q import quantize_weight_blockwise_batched

@@ -135,6 +135,27 @@ def main():
                     rec.update({"graph_ms": round(tg, 4), "graph_GBps": round(by / (tg * 1e-3) / 1e9, 1),
                                 "graph_frac_hbm": round(by / (tg * 1e-3) / 1e9 / HBM, 4)})
                 print(json.dumps(rec))
+    if args.what in ("all", "fanout"):
+        # NEXT-1: one Qwen3-8B layer's requant (4 weights, one launch) stored to R destinations
+        from paper_2601_18150_b200.sync import TensorSpec, local_replica_buffers
+        specs = [TensorSpec(nm, n, k) for nm, (n, k) in synth.QWEN3_8B_LINEARS.items()]
+        ws = {sp.name: (torch.randn((sp.n, sp.k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+              for sp in specs}
+        elems = sum(sp.n * sp.k for sp in specs)
+        for R in (1, 2, 4, 8):
+            from paper_2601_18150_b200.sync import WeightSyncEngine
+            eng = WeightSyncEngine(specs, dev, peers=local_replica_buffers(specs, dev, R))
+            step = [0]
+
+            def run():
+                step[0] += 1
+                eng.sync_step(step[0], ws)
+            t, lo, hi = timeit(run, args.iters, flush)
+            by = elems * (2 + R * (1 + 4 / 16384))
+            print(json.dumps({"kernel": "quantize_weight_blockwise_fanout", "destinations": R, "elements": elems,
+                              "ms": round(t, 4), "GBps": round(by / (t * 1e-3) / 1e9, 1),
+                              "frac_hbm": round(by / (t * 1e-3) / 1e9 / HBM, 4)}))
+            del eng
     if args.what in ("all", "mx"):
         # NEXT-4: MXFP8 quantizer (2 + 1 + 1/32 B per element) and block-scaled GEMM, Qwen3-8B M = 8192
         M = 8192
