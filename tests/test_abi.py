@@ -34,7 +34,8 @@ def test_header_declares_the_boundary():
                      "fp8_block_gemm_grouped_workspace_size", "fp8q_status_string", "fp8q_version",
                      "fp8q_kernel_launches", "rmsnorm_quantize_act_per_token_group",
                      "silu_mul_quantize_act_per_token_group", "kv_amax_update", "kv_scale_from_amax",
-                     "kv_quantize_append"]:
+                     "kv_quantize_append", "quantize_weight_blockwise_fanout", "mx_scale_bytes", "mx_quantize",
+                     "fp8_mx_gemm"]:
         assert required in names
 
 
@@ -83,6 +84,16 @@ def test_validation_paths_without_gpu(lib):
     assert lib.kv_quantize_append(fake, 8, 1024, 1024, fake, None, fake, 1024, 4, None, None, None) == 2
     assert lib.kv_quantize_append(fake, 8, 1024, 1024, odd, fake, fake, 1024, 4, None, None, None) == 3
     assert lib.kv_quantize_append(fake, 8, 1024, 1024, fake, fake, fake, 512, 16, None, None, None) == 1
+    # NEXT-4 MXFP8: k % 128 -> ESHAPE; n % 256 -> ESHAPE; scale bytes per (128 rows, k-block) = 512
+    assert lib.mx_scale_bytes(300, 4096) == 3 * 32 * 512 and lib.mx_scale_bytes(4, 100) == 0
+    assert lib.mx_quantize(fake, 4, 200, 200, fake, 200, fake, None, None) == 2
+    assert lib.fp8_mx_gemm(fake, 128, fake, fake, 128, fake, fake, 128, 0, 4, 128, 128, None) == 2
+    # NEXT-1 fan-out: no destination -> EINVAL; misaligned delta -> EALIGN
+    from paper_2601_18150_b200.fp8q import WeightTensorDesc
+    arr = (WeightTensorDesc * 1)(WeightTensorDesc(0x10000, 128, 256, 256, 0x10000, 256, 0x10000, 2))
+    d0 = (ctypes.c_int64 * 2)(0, 8)
+    assert lib.quantize_weight_blockwise_fanout(arr, 1, 0, d0, d0, None, None) == 1
+    assert lib.quantize_weight_blockwise_fanout(arr, 1, 2, d0, d0, None, None) == 3
 
 
 def test_product_package_never_imports_oracle():
