@@ -71,7 +71,12 @@ struct SkCfg {
     static constexpr int SA_BYTES = MT * 4;                          // TMA box bytes
     static constexpr int SA_SLOT = SA_BYTES < 128 ? 128 : SA_BYTES;  // TMA smem dst: 128-B aligned
     static constexpr int STAGE_BYTES = W_TILE + X_TILE;
-    static constexpr int STAGES_RAW = SK_SMEM_BUDGET / (STAGE_BYTES + SA_SLOT);
+    // MT <= 32: half the smem, registers and TMEM, so two CTAs -- this GEMM's and the next
+    // one's (programmatic dependent launch) -- fit on an SM and the next GEMM's weight stream
+    // starts while this one drains
+    static constexpr bool LIGHT = MT <= 32;
+    static constexpr int BUDGET = LIGHT ? SK_SMEM_BUDGET / 2 : SK_SMEM_BUDGET;
+    static constexpr int STAGES_RAW = BUDGET / (STAGE_BYTES + SA_SLOT);
     static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
     static constexpr int NBUF_RAW = 512 / MT;
     static constexpr int NBUF = NBUF_RAW > 8 ? 8 : NBUF_RAW;  // TMEM partial buffers
@@ -198,7 +203,7 @@ __device__ __forceinline__ void sk_store(const SkParams& p, int64_t n_row, int j
 }
 
 template <int MT>
-__global__ void __launch_bounds__(SK_THREADS, 1)
+__global__ void __launch_bounds__(SK_THREADS, SkCfg<MT>::LIGHT ? 2 : 1)
     fp8_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                            const __grid_constant__ CUtensorMap tmS, const SkParams p) {
     using C = SkCfg<MT>;
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     // let the next kernel in the stream (launched with programmatic stream serialization)
     // start its prologue and weight prefetch on SMs this grid vacates
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (warp < SK_EPI_WARP0) regs_dec<SK_REGS_CTRL>();
+    if (!C::LIGHT && warp < SK_EPI_WARP0) regs_dec<SK_REGS_CTRL>();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -273,6 +278,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                     }
             }
             grid_dependency_wait();
+            sk_trace(p, 0, 7);  // dev timeline: the previous grid has completed
             while (seg.next(p, tile, kb0, kb1)) {
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
@@ -324,7 +330,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         }
     } else if (warp >= SK_EPI_WARP0) {
         // ---------------------------------------------------------------- promotion warps
-        regs_inc<SK_REGS_EPI>();
+        if (!C::LIGHT) regs_inc<SK_REGS_EPI>();
         grid_dependency_wait();  // before any global write (D, workspace): the previous grid is done
         const int qd = warp & 3;                       // TMEM lane quarter of this warp
         const int h = (warp - SK_EPI_WARP0) >> 2;      // token-column half

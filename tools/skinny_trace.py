@@ -26,9 +26,12 @@ tr = torch.zeros(96 * 12 + 512, dtype=torch.int32, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 for _ in range(3):
     fp8q.fp8_block_gemm(xq, xs, wq, ws)
-lib.fp8q_debug_set_gemm_trace(tr.data_ptr())
+wq2 = wq.clone()
 flush.view(torch.int64).sum()
 torch.cuda._sleep(400_000)
+if "--pair" in sys.argv:  # a first GEMM (untraced) right before the traced one: PDL overlap
+    fp8q.fp8_block_gemm(xq, xs, wq2, ws)
+lib.fp8q_debug_set_gemm_trace(tr.data_ptr())
 fp8q.fp8_block_gemm(xq, xs, wq, ws)
 torch.cuda.synchronize()
 lib.fp8q_debug_set_gemm_trace(None)
@@ -43,7 +46,7 @@ print(f"CTAs {len(live)}: entry ns min/med/max {ent.min()}/{int(np.median(ent))}
 print("exit histogram (us):", np.histogram(ext / 1000, bins=8)[0].tolist(), np.round(np.histogram(ext / 1000, bins=8)[1], 1).tolist())
 base = t[0, 4]
 rel = (t - base) % (1 << 32)
-print(f"entry 0  setup_done {rel[0, 5]}  exit {rel[0, 6]}")
+print(f"entry 0  setup_done {rel[0, 5]}  dependency_wait_done {rel[0, 7]}  exit {rel[0, 6]}")
 print("it   issue   full   tfull   done   full-issue  tfull-full  done-tfull")
 last = int(np.max(np.nonzero(t[:, 0])[0])) if np.any(t[:, 0]) else -1
 for i in range(last + 1):
