@@ -254,10 +254,12 @@ def test_skinny_decode_vs_oracle(m, n, k):
     assert torch.equal(_run(a, sa, b, sb).view(torch.int32), y.view(torch.int32))
 
 
-def test_skinny_matches_tile_kernel_when_scales_misaligned():
+@pytest.mark.parametrize("m,with_ws", [(24, False), (8, True), (3, True)])
+def test_skinny_matches_tile_kernel_when_scales_misaligned(m, with_ws):
     # activation scales at a pointer that is not 16-byte aligned cannot be TMA-loaded: the call
-    # falls back to the tile kernel (no split: no workspace), whose result must agree
-    m, n, k = 24, 768, 1024
+    # falls back to the one-CTA tile kernel, whose result must agree; with a workspace and
+    # M <= 16 that kernel splits K (deterministic serial fixup)
+    n, k = 768, 1024
     a, sa, b, sb = _operands(m, n, k, 61)
     y = _run(a, sa, b, sb)
     ld = fp8q.act_scales_ld(m)
@@ -267,9 +269,12 @@ def test_skinny_matches_tile_kernel_when_scales_misaligned():
     lib = fp8q.load_library()
     yt = torch.empty((m, n), dtype=torch.float32, device="cuda")
     da, db, dsb = (torch.from_numpy(t).cuda() for t in (a, b, sb))  # held until the kernel ran
-    st = lib.fp8_block_gemm(da.data_ptr(), k, big.data_ptr() + 4, ld + 4, db.data_ptr(), k, dsb.data_ptr(),
-                            sb.shape[1], yt.data_ptr(), n, 1, m, n, k, None, 0,
-                            torch.cuda.current_stream().cuda_stream)
-    torch.cuda.synchronize()
-    assert st == 0
-    assert rel_frobenius(yt.cpu().numpy(), y.cpu().numpy()) <= 1e-6
+    wsb = int(lib.fp8_block_gemm_workspace_size(m, n, k)) if with_ws else 0
+    ws = torch.zeros(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    for _ in range(2):  # twice: the workspace must be left reusable
+        st = lib.fp8_block_gemm(da.data_ptr(), k, big.data_ptr() + 4, ld + 4, db.data_ptr(), k, dsb.data_ptr(),
+                                sb.shape[1], yt.data_ptr(), n, 1, m, n, k, ws.data_ptr() if wsb else None, wsb,
+                                torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert st == 0
+        assert rel_frobenius(yt.cpu().numpy(), y.cpu().numpy()) <= 1e-6
