@@ -231,7 +231,10 @@ __device__ __forceinline__ int split_begin(const KParams& p, int s) {
 // For every k-block: wait for the partial in TMEM buffer it % NBUF, tcgen05.ld it, hand the
 // buffer back (to the leader CTA of a pair when PAIR), and
 // acc += P_kb * (sa[kb][row] * sb[col0/128][kb]) with packed FFMA2; then store the tile.
-template <int BN, int NBUF, bool PAIR>
+// SPLIT (CTA pair only): the partial of k-block `it` arrives as two 128-column slots, one per
+// column half h, in a ring of NBUF slots: slot 2*it + h.  Each half's promotion warps wait
+// only for their own half's MMAs and release only their slot.
+template <int BN, int NBUF, bool PAIR, bool SPLIT = false>
 __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap* tmD, uint8_t* stg,
                                              const EpiTile& tile, const ScalePre& pre, bool has_next,
                                              const EpiTile& next, ScalePre& next_pre, uint32_t tmem,
@@ -266,8 +269,9 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
             sb1 = __ldg(sbp + kb + 2);
         }
         if (kb == (kb1 - kb0 > 4 ? kb1 - 4 : kb0)) next_pre = load_scales(nq);
-        const uint32_t buf = it % NBUF;
-        const uint32_t bph = (it / NBUF) & 1u;
+        const uint32_t slot = SPLIT ? 2u * it + static_cast<uint32_t>(h) : it;
+        const uint32_t buf = slot % NBUF;
+        const uint32_t bph = (slot / NBUF) & 1u;
         mbar_wait(&tfull[buf], bph);
         tc_fence_after();
         const bool tr = (threadIdx.x == EPI_WARP0 * 32);
@@ -283,7 +287,8 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
             }
             continue;
         }
-        const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * BN + h * EPI_COLS;
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) +
+                               (SPLIT ? buf * EPI_COLS : buf * BN + h * EPI_COLS);
         // Software-pipelined: the tcgen05.ld of chunk c+1 is in flight while chunk c's FMAs
         // issue, so each TMEM load latency after the first overlaps useful work.
         float v[2][32];
@@ -670,24 +675,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // leader (both CTAs' TMA bytes + the peer's arrival land there); empty[s] and tfull[b] are
 // arrived in both CTAs by a multicast tcgen05.commit; tempty[b] lives in the leader and
 // collects the 16 promotion warps of the pair.
-template <int PBN>
+// SPLIT: the tile's k-block is issued as two N = PBN/2 MMA groups, one per column half, each
+// committed to its own TMEM slot (NBUF slots of PBN/2 columns), so a half's promotion warps
+// start reading after half the MMA time and the tensor core can run up to NBUF-1 slots ahead
+// of the slowest reader.  Each CTA then holds, per half, PBN/4 B rows: CTA r loads rows
+// [h*PBN/2 + r*PBN/4, +PBN/4) of the tile into its smem half h, so the N = PBN/2 pair MMA
+// (first PBN/4 rows from the leader, next PBN/4 from the peer) covers columns h*PBN/2.. in order.
+template <int PBN, bool SPLIT = false>
 struct PairCfg {
-    static constexpr int BN = PBN;          // MMA N (tile columns)
+    static constexpr int BN = PBN;          // tile columns
     static constexpr int B_HALF = PBN / 2;  // B rows loaded by each CTA
+    static constexpr int B_BOX = SPLIT ? PBN / 4 : PBN / 2;  // B rows per TMA box
     static constexpr int STAGE_BYTES = A_TILE + B_HALF * BK;  // per CTA
     static constexpr int STAGES = SMEM_BUDGET / STAGE_BYTES;
-    static constexpr int NBUF = TMEM_COLS / PBN;
-    static constexpr uint32_t IDESC = idesc_e4m3_f32(2 * BM, PBN);
+    static constexpr int NBUF = SPLIT ? TMEM_COLS / (PBN / 2) : TMEM_COLS / PBN;
+    static constexpr uint32_t IDESC = idesc_e4m3_f32(2 * BM, SPLIT ? PBN / 2 : PBN);
     static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + EPI_STAGE_BYTES + 512;
 };
 constexpr int PAIR_RASTER_GM = 8;  // pair m-tiles (256 rows) per raster band
 
-template <int PBN>
+template <int PBN, bool SPLIT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     fp8_block_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                                const __grid_constant__ CUtensorMap tmB,
                                const __grid_constant__ CUtensorMap tmD, const KParams p) {
-    using PC = PairCfg<PBN>;
+    using PC = PairCfg<PBN, SPLIT>;
     constexpr int STAGES = PC::STAGES;
     constexpr int NBUF = PC::NBUF;
     constexpr int PAIR_BN = PC::BN;
@@ -723,7 +735,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);                  // multicast commit
-            mbar_init(&tempty[b], 2 * NUM_EPI_WARPS);  // leader: promotion warps of both CTAs
+            // leader: the promotion warps of both CTAs (SPLIT: of one column half)
+            mbar_init(&tempty[b], SPLIT ? NUM_EPI_WARPS : 2 * NUM_EPI_WARPS);
         }
         for (int hh = 0; hh < 2; ++hh) {
             mbar_init(&stg_full[hh], 4);
@@ -761,7 +774,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     else
                         mbar_arrive_cluster(&full[stage], 0);
                     tma_load_2d_pair(smA + stage * A_TILE, &tmA, &full[stage], kb * BK, arow);
-                    tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK), &tmB, &full[stage], kb * BK, brow, cur.g);
+                    if (SPLIT) {
+                        const int32_t b0 = nt * PAIR_BN + static_cast<int32_t>(rank) * PC::B_BOX;
+                        tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK), &tmB, &full[stage], kb * BK, b0, cur.g);
+                        tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK) + PC::B_BOX * BK, &tmB, &full[stage],
+                                         kb * BK, b0 + PAIR_BN / 2, cur.g);
+                    } else {
+                        tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK), &tmB, &full[stage], kb * BK, brow, cur.g);
+                    }
                 }
             }
         }
@@ -777,6 +797,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
+                    if (SPLIT) {
+                        mbar_wait(&full[stage], ph);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(smA + stage * A_TILE);
+                        const uint32_t b0 = smem_u32(smB + stage * (PAIR_B_HALF * BK));
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const uint32_t slot = 2u * it + hh;
+                            const uint32_t buf = slot % NBUF;
+                            mbar_wait(&tempty[buf], ((slot / NBUF) & 1u) ^ 1u);
+                            tc_fence_after();
+                            if (hh == 0) trace_ev(p, it, 1);
+                            const uint32_t d = tmem + buf * (PAIR_BN / 2);
+                            const uint32_t bh = b0 + hh * (PC::B_BOX * BK);
+#pragma unroll
+                            for (int kk = 0; kk < BK / 32; ++kk)
+                                mma_f8f6f4_pair(d, smem_desc_k_sw128(a0 + kk * 32), smem_desc_k_sw128(bh + kk * 32),
+                                                PAIR_IDESC, kk > 0 ? 1u : 0u);
+                            mma_commit_pair(&tfull[buf], 0x3);
+                        }
+                        mma_commit_pair(&empty[stage], 0x3);
+                        continue;
+                    }
                     const uint32_t buf = it % NBUF;
                     const uint32_t bph = (it / NBUF) & 1u;
                     mbar_wait(&tempty[buf], bph ^ 1u);
@@ -796,8 +839,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             // the peer's last remote arrivals must land before the barriers go away
-            for (uint32_t j = 0; j < NBUF && j < it; ++j) {
-                const uint32_t i = it - 1 - j;
+            const uint32_t slots = SPLIT ? 2u * it : it;
+            for (uint32_t j = 0; j < NBUF && j < slots; ++j) {
+                const uint32_t i = slots - 1 - j;
                 mbar_wait(&tempty[i % NBUF], (i / NBUF) & 1u);
             }
         }
@@ -842,7 +886,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const bool have_next = cur.seek(p, tn, mt, nt);
             const EpiTile next = have_next ? make_tile(mt, nt) : tile;
             ScalePre next_pre = pre;
-            promote_tile<PAIR_BN, NBUF, true>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd,
+            promote_tile<PAIR_BN, NBUF, true, SPLIT>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd,
                                               h, lane, tfull, tempty, it, stg_full, stg_empty, tile_no);
             tile = next;
             pre = next_pre;
@@ -906,6 +950,9 @@ cudaError_t device_info(int& sms) {
         e = cudaFuncSetAttribute(fp8_block_gemm_pair_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(PairCfg<128>::SMEM_BYTES));
         if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(fp8_block_gemm_pair_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(PairCfg<256, true>::SMEM_BYTES));
+        if (e != cudaSuccess) return e;
         di.attr_set = true;
     }
     sms = di.sms;
@@ -949,7 +996,7 @@ int choose_kind(const GemmArgs& a) {
         const char* e = std::getenv("FP8Q_GEMM_KIND");
         return e ? std::atoi(e) : 0;
     }();
-    if (forced == 128 || forced == 256 || forced == 1128 || forced == 1256) return forced;
+    if (forced == 128 || forced == 256 || forced == 1128 || forced == 1256 || forced == 2256) return forced;
     // Measured (tools/kernel_bench.py --moe, Qwen3-30B-A3B experts): the grouped GEMM's short
     // per-expert k-loops (fc2: 6 k-blocks) and ragged segments favour the one-CTA 128 x 256
     // tile (+5 % at T = 8192, +34-41 % at T = 1024) over the CTA pair.
@@ -958,13 +1005,15 @@ int choose_kind(const GemmArgs& a) {
     return 1256;
 }
 
-// kind: 128 / 256 = one-CTA kernel with that BN; 1128 / 1256 = CTA-pair kernel, 256 x BN tiles.
+// kind: 128 / 256 = one-CTA kernel with that BN; 1128 / 1256 = CTA-pair kernel, 256 x BN tiles;
+// 2256 = CTA-pair kernel, 256 x 256 tiles committed per 128-column half (PairCfg SPLIT).
 template <int KIND>
 cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encode, int sms,
                        cudaStream_t stream) {
     constexpr bool kPair = KIND > 1000;
-    constexpr int BN = kPair ? KIND - 1000 : KIND;
-    constexpr int B_BOX = kPair ? BN / 2 : KIND;
+    constexpr bool kSplit = KIND > 2000;
+    constexpr int BN = kSplit ? KIND - 2000 : (kPair ? KIND - 1000 : KIND);
+    constexpr int B_BOX = kSplit ? BN / 4 : (kPair ? BN / 2 : KIND);
     CUtensorMap tmA, tmB;
     {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.m)};
@@ -1058,8 +1107,8 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
             const int64_t tiles = ((a.m + 2 * BM - 1) / (2 * BM)) * p.num_n_tiles;
             clusters = tiles < clusters ? tiles : clusters;
         }
-        fp8_block_gemm_pair_kernel<BN><<<static_cast<unsigned>(2 * clusters), NUM_THREADS,
-                                         PairCfg<BN>::SMEM_BYTES, stream>>>(tmA, tmB, tmD, p);
+        fp8_block_gemm_pair_kernel<BN, kSplit><<<static_cast<unsigned>(2 * clusters), NUM_THREADS,
+                                                 PairCfg<BN, kSplit>::SMEM_BYTES, stream>>>(tmA, tmB, tmD, p);
     } else {
         int64_t grid = sms;
         if (a.offsets == nullptr) {
@@ -1105,6 +1154,7 @@ cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* l
         case 128: e = launch_cfg<128>(a, encode, sms, stream); break;
         case 256: e = launch_cfg<256>(a, encode, sms, stream); break;
         case 1128: e = launch_cfg<1128>(a, encode, sms, stream); break;
+        case 2256: e = launch_cfg<2256>(a, encode, sms, stream); break;
         default: e = launch_cfg<1256>(a, encode, sms, stream); break;
     }
     if (e == cudaSuccess) *launches = 1;
