@@ -18,6 +18,7 @@
 //     x = -0 still gives -0 (IEEE: -0 / s = -0).  Blocks below the guard use div.rn;
 //   * packed cvt.rn.satfinite.e4m3x2.f32 (RNE, saturating, reading Q1/Q7), 8-byte stores.
 #include <cstdint>
+#include <cstdlib>
 
 #include "ptx.cuh"
 #include "quant_kernels.h"
@@ -394,10 +395,9 @@ __device__ __forceinline__ void aq_load(const uint16_t* __restrict__ x, int64_t 
 }
 __device__ __forceinline__ void aq_process(const AItemRegs& d, uint8_t* __restrict__ q, int64_t ld_q,
                                            float* __restrict__ scales, int64_t ld_s, int64_t groups,
-                                           int64_t chunks, int64_t item, int32_t* __restrict__ nonfinite_flag,
+                                           int64_t row, int64_t chunk, int32_t* __restrict__ nonfinite_flag,
                                            const ScaleTables& tabs) {
     const int lane = threadIdx.x & 31;
-    const int64_t row = item / chunks, chunk = item - (item / chunks) * chunks;
     uint32_t ab[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) ab[j] = abs_max_bits16(d.v[j]);
@@ -442,13 +442,133 @@ __global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
     while (item < items) {
         int64_t nxt = item + warps;
         if (nxt < items) aq_load(x, ld_x, groups, chunks, nxt, b);
-        aq_process(a, q, ld_q, scales, ld_s, groups, chunks, item, nonfinite_flag, tabs);
+        aq_process(a, q, ld_q, scales, ld_s, groups, item / chunks, item % chunks, nonfinite_flag, tabs);
         item = nxt;
         if (item >= items) break;
         nxt = item + warps;
         if (nxt < items) aq_load(x, ld_x, groups, chunks, nxt, a);
-        aq_process(b, q, ld_q, scales, ld_s, groups, chunks, item, nonfinite_flag, tabs);
+        aq_process(b, q, ld_q, scales, ld_s, groups, item / chunks, item % chunks, nonfinite_flag, tabs);
         item = nxt;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Activations, bulk-staged path (production): one persistent CTA per SM owns an EQUAL
+// contiguous range of items (item = token row x 16 groups = 2048 channels = 4 KB), so no SM
+// finishes a whole item early (the warp-persistent grid above leaves a 1/7 tail at M = 8192,
+// K = 4096).  A producer thread streams the range into a ring of ABQ_STAGES shared-memory stages
+// of ABQ_ITEMS items with cp.async.bulk (one bulk copy per item, completion counted in bytes
+// on the stage's mbarrier): up to ABQ_STAGES x 32 KB of HBM reads in flight per SM, issued by
+// one thread.  Two teams of ABQ_ITEMS consumer warps take alternate stages; each warp encodes
+// one item from shared memory exactly as the wide path does (same registers, same arithmetic)
+// and releases the stage with one arrive.
+constexpr int ABQ_ITEMS = 8;    // items per stage (one per warp of a team)
+constexpr int ABQ_TEAMS = 2;    // consumer teams (alternate stages)
+constexpr int ABQ_STAGES = 6;   // ring depth: 6 x 32 KB
+constexpr int ABQ_ITEM_BYTES = 4096;
+constexpr int ABQ_THREADS = (ABQ_ITEMS * ABQ_TEAMS + 1) * 32;
+constexpr size_t ABQ_SMEM = size_t(ABQ_STAGES) * ABQ_ITEMS * ABQ_ITEM_BYTES + 2 * ABQ_STAGES * 8 + 128;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)),
+        "l"(0x12F0000000000000ull)  // L2 evict_first: every byte is read exactly once
+        : "memory");
+}
+__device__ __forceinline__ void aq_load_smem(uint32_t base, int64_t groups, int64_t chunk, AItemRegs& d) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t g = chunk * 16 + 4 * j + (lane >> 3);
+        if (g < groups) {
+            const uint32_t a = base + static_cast<uint32_t>((4 * j + (lane >> 3)) * 256 + (lane & 7) * 32);
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(d.v[j][0]), "=r"(d.v[j][1]), "=r"(d.v[j][2]), "=r"(d.v[j][3]) : "r"(a));
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(d.v[j][4]), "=r"(d.v[j][5]), "=r"(d.v[j][6]), "=r"(d.v[j][7]) : "r"(a + 16));
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) d.v[j][t] = 0u;
+        }
+    }
+}
+__global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kernel(
+    const uint16_t* __restrict__ x, int64_t ld_x, uint8_t* __restrict__ q, int64_t ld_q,
+    float* __restrict__ scales, int64_t ld_s, int64_t groups, int64_t chunks, int64_t items,
+    int32_t* __restrict__ nonfinite_flag) {
+    extern __shared__ __align__(128) uint8_t abq_smem[];
+    __shared__ ScaleTables tabs;
+    uint64_t* full = reinterpret_cast<uint64_t*>(abq_smem + size_t(ABQ_STAGES) * ABQ_ITEMS * ABQ_ITEM_BYTES);
+    uint64_t* empty = full + ABQ_STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // this CTA's equal share of the items
+    const int64_t i0 = items * blockIdx.x / gridDim.x;
+    const int64_t i1 = items * (blockIdx.x + 1) / gridDim.x;
+    const int64_t nstages = (i1 - i0 + ABQ_ITEMS - 1) / ABQ_ITEMS;
+    init_scale_tables(tabs);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ABQ_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], ABQ_ITEMS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t ring = smem_u32(abq_smem);
+    if (warp == ABQ_ITEMS * ABQ_TEAMS) {
+        if (lane == 0) {
+            // (row, chunk) of the current item, advanced incrementally (no 64-bit division)
+            int64_t row = i0 / chunks;
+            int32_t chunk = static_cast<int32_t>(i0 - row * chunks);
+            const int32_t nch = static_cast<int32_t>(chunks);
+            const uint32_t tail_bytes = static_cast<uint32_t>(groups - (chunks - 1) * 16) * 256u;
+            int64_t left = i1 - i0;
+            uint32_t s = 0, ph = 0;
+            while (left > 0) {
+                mbar_wait(&empty[s], ph ^ 1u);
+                const int cnt = left < ABQ_ITEMS ? static_cast<int>(left) : ABQ_ITEMS;
+                uint32_t bytes = 0;
+                for (int j = 0; j < cnt; ++j) {
+                    // copies may complete before the expect_tx below: the phase cannot, since
+                    // its one arrival (the expect_tx arrive) is still pending
+                    const uint32_t nb = chunk == nch - 1 ? tail_bytes : 4096u;
+                    bulk_g2s(ring + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, x + row * ld_x + chunk * 2048, nb,
+                             &full[s]);
+                    bytes += nb;
+                    if (++chunk == nch) {
+                        chunk = 0;
+                        ++row;
+                    }
+                }
+                mbar_arrive_expect_tx(&full[s], bytes);
+                left -= cnt;
+                if (++s == ABQ_STAGES) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    const int team = warp / ABQ_ITEMS, w = warp % ABQ_ITEMS;
+    for (int64_t it = team; it < nstages; it += ABQ_TEAMS) {
+        const uint32_t s = static_cast<uint32_t>(it % ABQ_STAGES);
+        mbar_wait(&full[s], static_cast<uint32_t>((it / ABQ_STAGES) & 1));
+        const int64_t item = i0 + it * ABQ_ITEMS + w;
+        if (item < i1) {
+            // 32-bit (the host keeps items < 2^31 on this path): once per 4 KB item
+            const int64_t row = static_cast<uint32_t>(item) / static_cast<uint32_t>(chunks);
+            const int64_t chunk = item - row * chunks;
+            AItemRegs d;
+            aq_load_smem(ring + (s * ABQ_ITEMS + w) * ABQ_ITEM_BYTES, groups, chunk, d);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // the item is in registers: free the slot
+            aq_process(d, q, ld_q, scales, ld_s, groups, row, chunk, nonfinite_flag, tabs);
+        } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
     }
 }
 
@@ -556,7 +676,30 @@ cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, 
     if (items == 0) return cudaSuccess;
     const int64_t blocks = (items + 7) / 8;
     if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
-    if (al(x, 32) && ld_x % 16 == 0 && al(q, 16) && ld_q % 16 == 0) {
+    static const int act_kernel = [] {  // dev: FP8Q_ACT_KERNEL=wide selects the warp-persistent path
+        const char* e = std::getenv("FP8Q_ACT_KERNEL");
+        return (e != nullptr && e[0] == 'w') ? 1 : 0;
+    }();
+    if (act_kernel == 0 && al(x, 16) && ld_x % 8 == 0 && al(q, 16) && ld_q % 16 == 0 &&
+        m * ((groups + 15) / 16) < (1LL << 31)) {
+        static bool attr_done[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && !attr_done[dev]) {
+            const cudaError_t ea = cudaFuncSetAttribute(act_per_token_group_bulk_kernel,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        static_cast<int>(ABQ_SMEM));
+            if (ea != cudaSuccess) return ea;
+            attr_done[dev] = true;
+        }
+        const int64_t wchunks = (groups + 15) / 16;
+        const int64_t witems = m * wchunks;
+        const int64_t per_cta_min = 2 * ABQ_ITEMS;  // small inputs: fewer CTAs, each a few stages
+        int64_t grid = (witems + per_cta_min - 1) / per_cta_min;
+        grid = grid < sm_count() ? grid : sm_count();
+        act_per_token_group_bulk_kernel<<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
+            x, ld_x, q, ld_q, scales, ld_s, groups, wchunks, witems, flag);
+    } else if (al(x, 32) && ld_x % 16 == 0 && al(q, 16) && ld_q % 16 == 0) {
         const int64_t wchunks = (groups + 15) / 16;
         const int64_t witems = m * wchunks;
         const int64_t wblocks = (witems + 7) / 8;

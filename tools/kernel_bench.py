@@ -116,6 +116,12 @@ def main():
             gbs = M * k * (3 + 4 / 128) / (t * 1e-3) / 1e9
             print(json.dumps({"kernel": "quantize_act_per_token_group", "shape": [M, k], "ms": round(t, 4),
                               "p10": round(lo, 4), "p90": round(hi, 4), "GBps": round(gbs, 1), "frac_hbm": round(gbs / HBM, 4)}))
+        if args.what in ("aqref",):
+            # reference point for an HBM-bound 2 B -> 1 B element map: torch's own cast kernel
+            t, lo, hi = timeit(lambda: x.to(torch.float8_e4m3fn), args.iters, flush)
+            gbs = M * k * 3 / (t * 1e-3) / 1e9
+            print(json.dumps({"kernel": "torch_cast_bf16_to_e4m3", "shape": [M, k], "ms": round(t, 4),
+                              "GBps": round(gbs, 1), "frac_hbm": round(gbs / HBM, 4)}))
         if args.what in ("all", "gemm"):
             t, lo, hi = timeit(lambda: fp8q.fp8_block_gemm(xq, xs, wq, ws, out=y), args.iters, flush)
             tf = 2 * M * n * k / (t * 1e-3) / 1e12
