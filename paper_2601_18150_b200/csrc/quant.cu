@@ -17,6 +17,9 @@
 //     (x, amax) map in tests/test_gpu_exhaustive.py); the sign is re-imposed from x so that
 //     x = -0 still gives -0 (IEEE: -0 / s = -0).  Blocks below the guard use div.rn;
 //   * packed cvt.rn.satfinite.e4m3x2.f32 (RNE, saturating, reading Q1/Q7), 8-byte stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 #include <cstdlib>
 
@@ -253,6 +256,8 @@ struct WTensor {
     int64_t blk0;  // first global block index of this tensor
 };
 struct WBatch {
+    // bulk path: one 2-D tensor map per tensor (BF16 [n][k], box 128 x 128, zero OOB fill)
+    CUtensorMap tm[kMaxWeightBatch];
     WTensor t[kMaxWeightBatch];
     int count;
     int64_t nblocks;
@@ -292,8 +297,9 @@ template <bool kFanout>
 __device__ __forceinline__ void wq_process(const WBlockRegs& d, int64_t n, int64_t k, uint8_t* __restrict__ q,
                                            int64_t ld_q, float* __restrict__ scales, int64_t ld_s,
                                            int64_t nbk, int64_t blk, uint32_t* red,
-                                           int32_t* __restrict__ nonfinite_flag, const WBatch& bt) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                           int32_t* __restrict__ nonfinite_flag, const WBatch& bt,
+                                           int warp = threadIdx.x >> 5, int bar_id = 0) {
+    const int lane = threadIdx.x & 31;
     const int64_t bi = blk / nbk, bj = blk - (blk / nbk) * nbk;
     const int64_t col = bj * 128 + (lane & 7) * 16;
     const int64_t row0 = bi * 128 + warp * 16 + (lane >> 3);
@@ -302,12 +308,15 @@ __device__ __forceinline__ void wq_process(const WBlockRegs& d, int64_t n, int64
     for (int i = 0; i < 4; ++i) ab = max(ab, abs_max_bits16(d.v[i]));
     ab = __reduce_max_sync(0xFFFFFFFFu, ab);
     if (lane == 0) red[warp] = ab;
-    __syncthreads();
+    if (bar_id == 0)
+        __syncthreads();
+    else  // the 8 warps of one consumer team (bulk kernel)
+        asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory");
     ab = red[0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) ab = max(ab, red[i]);
     const float s = scale_from_amax_bits(ab);
-    if (threadIdx.x == 0) {
+    if (warp == 0 && lane == 0) {
         if (kFanout) {
             for (int dd = 0; dd < bt.ndest; ++dd)
                 *reinterpret_cast<float*>(reinterpret_cast<char*>(scales + bi * ld_s + bj) + bt.ds[dd]) = s;
@@ -572,6 +581,133 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Weights, bulk-staged path (production for the wide layout): one persistent CTA per SM owns
+// an EQUAL contiguous range of the batch's 128x128 blocks (the block-strided grid above ends
+// with a partial wave: 1024 blocks over 296 CTAs is 3.46 waves for o_proj).  A producer warp
+// streams the range into a ring of WBQ_STAGES 32 KB shared-memory stages, one block per stage,
+// with ONE 2-D TMA load per block (box 128 x 128 BF16 of the tensor's map, rows past n and
+// columns past k zero-filled, completion counted in bytes on the stage's mbarrier), so up to 6
+// blocks of HBM reads are in flight per SM.  (Per-row cp.async.bulk copies of 256 B were
+// measured at a quarter of this rate: the copy engine is bound by requests, not bytes.)  Two teams of 8 consumer warps take alternate stages; a team reads its
+// block from shared memory into exactly the registers the wide path loads from global memory,
+// frees the stage, and runs the same wq_process (same arithmetic, same stores) with the block
+// amax reduced over the team's named barrier.
+constexpr int WBQ_STAGES = 6;
+constexpr int WBQ_TEAMS = 2;
+constexpr int WBQ_BLOCK_BYTES = 128 * 256;
+constexpr int WBQ_THREADS = (8 * WBQ_TEAMS + 1) * 32;
+constexpr size_t WBQ_SMEM = size_t(WBQ_STAGES) * WBQ_BLOCK_BYTES + 2 * WBQ_STAGES * 8 + 128;
+
+// Thread (warp w of its team, lane l) takes rows 16w + 4i + (l >> 3), columns 16 (l & 7) .. +15
+// of the staged block (row r at byte 256 r): the 16-byte chunks 2j and 2j+1 (j = l & 7).  The
+// two loads visit them in the order (2j + h, 2j + 1 - h), h = j >> 2, so each 8-lane phase
+// touches 8 distinct bank quads (chunk mod 8 all different): conflict-free.
+__device__ __forceinline__ void wq_load_smem(uint32_t base, int64_t rows_in, int64_t cols_in, int warp,
+                                             WBlockRegs& d) {
+    const int lane = threadIdx.x & 31, j = lane & 7, h = j >> 2;
+    const bool col_ok = 16 * j < cols_in;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = warp * 16 + 4 * i + (lane >> 3);
+        if (col_ok && r < rows_in) {
+            const uint32_t a = base + static_cast<uint32_t>(r * 256);
+            uint32_t p0, p1, p2, p3, q0, q1, q2, q3;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(p0), "=r"(p1), "=r"(p2), "=r"(p3) : "r"(a + (2 * j + h) * 16));
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(q0), "=r"(q1), "=r"(q2), "=r"(q3) : "r"(a + (2 * j + 1 - h) * 16));
+            d.v[i][0] = h ? q0 : p0;
+            d.v[i][1] = h ? q1 : p1;
+            d.v[i][2] = h ? q2 : p2;
+            d.v[i][3] = h ? q3 : p3;
+            d.v[i][4] = h ? p0 : q0;
+            d.v[i][5] = h ? p1 : q1;
+            d.v[i][6] = h ? p2 : q2;
+            d.v[i][7] = h ? p3 : q3;
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) d.v[i][t] = 0u;
+        }
+    }
+}
+
+template <bool kFanout>
+__global__ void __launch_bounds__(WBQ_THREADS, 1) weight_blockwise_bulk_kernel(const __grid_constant__ WBatch bt,
+                                                                               int32_t* __restrict__ nonfinite_flag) {
+    extern __shared__ __align__(128) uint8_t wbq_smem[];
+    __shared__ uint32_t red[WBQ_TEAMS][2][8];
+    uint64_t* full = reinterpret_cast<uint64_t*>(wbq_smem + size_t(WBQ_STAGES) * WBQ_BLOCK_BYTES);
+    uint64_t* empty = full + WBQ_STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b0 = bt.nblocks * blockIdx.x / gridDim.x;
+    const int64_t b1 = bt.nblocks * (blockIdx.x + 1) / gridDim.x;
+    const int64_t nb = b1 - b0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < WBQ_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t ring = smem_u32(wbq_smem);
+    auto tensor_of = [&](int64_t blk) {
+        int i = 0;
+        while (i + 1 < bt.count && blk >= bt.t[i + 1].blk0) ++i;
+        return i;
+    };
+    if (warp == 8 * WBQ_TEAMS) {  // producer warp (one elected lane)
+        if (lane != 0) return;
+        int ti = nb > 0 ? tensor_of(b0) : 0;
+        int64_t bi = 0, bj = 0;
+        if (nb > 0) {
+            const int64_t local = b0 - bt.t[ti].blk0;
+            bi = local / bt.t[ti].nbk;
+            bj = local - bi * bt.t[ti].nbk;
+        }
+        uint32_t s = 0, ph = 0;
+        for (int64_t it = 0; it < nb; ++it) {
+            const WTensor& t = bt.t[ti];
+            mbar_wait(&empty[s], ph ^ 1u);
+            // the full box is counted even where it is zero-filled out of bounds
+            mbar_arrive_expect_tx(&full[s], WBQ_BLOCK_BYTES);
+            tma_load_2d_hint(wbq_smem + size_t(s) * WBQ_BLOCK_BYTES, &bt.tm[ti], &full[s],
+                             static_cast<int32_t>(bj * 128), static_cast<int32_t>(bi * 128),
+                             0x12F0000000000000ull);  // L2 evict_first: every byte is read once
+            if (++bj == t.nbk) {
+                bj = 0;
+                if (++bi * 128 >= t.n) {
+                    bi = 0;
+                    ++ti;
+                }
+            }
+            if (++s == WBQ_STAGES) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+        return;
+    }
+    const int team = warp >> 3, w = warp & 7;
+    int par = 0;
+    for (int64_t it = team; it < nb; it += WBQ_TEAMS) {
+        const uint32_t s = static_cast<uint32_t>(it % WBQ_STAGES);
+        const int64_t blk = b0 + it;
+        const WTensor& t = bt.t[tensor_of(blk)];
+        const int64_t local = blk - t.blk0;
+        const int64_t bi = local / t.nbk, bj = local - (local / t.nbk) * t.nbk;
+        mbar_wait(&full[s], static_cast<uint32_t>((it / WBQ_STAGES) & 1));
+        WBlockRegs d;
+        wq_load_smem(ring + s * WBQ_BLOCK_BYTES, t.n - bi * 128, t.k - bj * 128, w, d);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // the block is in registers: free the stage
+        wq_process<kFanout>(d, t.n, t.k, t.q, t.ld_q, t.scales, t.ld_s, t.nbk, local, red[team][par],
+                            nonfinite_flag, bt, w, 1 + team);
+        par ^= 1;
+    }
+}
+
 int sm_count() {
     static int sms = [] {
         int dev = 0, v = 148;
@@ -603,8 +739,46 @@ cudaError_t launch_weight_blockwise_batch(const WeightDesc* descs, int count, in
     if (ndest > 0)
         for (int i = 0; i < count; ++i)
             if (!wide_ok(descs[i])) return cudaErrorInvalidValue;  // fan-out runs on the wide path only
+    // dev/test override: FP8Q_WEIGHT_KERNEL=wide | bulk forces that path (default: by size)
+    static const int kernel_env = [] {
+        const char* e = std::getenv("FP8Q_WEIGHT_KERNEL");
+        return e == nullptr ? 0 : (e[0] == 'w' ? 1 : (e[0] == 'b' ? 2 : 0));
+    }();
+    const auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encode_fn());
+    // the bulk path wins on large batches (the per-layer sync launch: 11,776 blocks for a Qwen3-8B
+    // layer) and loses a few % on a single small tensor (qkv: 1,536 blocks, ~10 per SM), where the
+    // block-strided grid's register prefetch ramps up faster
+    int64_t total_blocks = 0;
+    for (int i = 0; i < count; ++i)
+        if (wide_ok(descs[i])) total_blocks += ((descs[i].n + 127) / 128) * ((descs[i].k + 127) / 128);
+    const bool bulk = encode != nullptr && kernel_env != 1 && (kernel_env == 2 || total_blocks >= 16LL * sm_count());
     auto flush = [&]() -> cudaError_t {
         if (bt.count == 0) return cudaSuccess;
+        if (bulk) {
+            static bool attr_done[64] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev >= 0 && dev < 64 && !attr_done[dev]) {
+                cudaError_t ea = cudaFuncSetAttribute(weight_blockwise_bulk_kernel<false>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      static_cast<int>(WBQ_SMEM));
+                if (ea == cudaSuccess)
+                    ea = cudaFuncSetAttribute(weight_blockwise_bulk_kernel<true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(WBQ_SMEM));
+                if (ea != cudaSuccess) return ea;
+                attr_done[dev] = true;
+            }
+            const int64_t grid = bt.nblocks < sm_count() ? bt.nblocks : sm_count();
+            if (bt.ndest > 0)
+                weight_blockwise_bulk_kernel<true><<<static_cast<unsigned>(grid), WBQ_THREADS, WBQ_SMEM, stream>>>(
+                    bt, flag);
+            else
+                weight_blockwise_bulk_kernel<false><<<static_cast<unsigned>(grid), WBQ_THREADS, WBQ_SMEM, stream>>>(
+                    bt, flag);
+            bt.count = 0;
+            bt.nblocks = 0;
+            return cudaGetLastError();
+        }
         const int64_t cap = 2LL * sm_count();
         const int64_t grid = bt.nblocks < cap ? bt.nblocks : cap;
         if (grid > 0) {
@@ -634,6 +808,17 @@ cudaError_t launch_weight_blockwise_batch(const WeightDesc* descs, int count, in
             t.ld_s = d.ld_s;
             t.nbk = nbk;
             t.blk0 = bt.nblocks;
+            if (bulk) {
+                cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.k), static_cast<cuuint64_t>(d.n)};
+                cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ld_w) * 2};
+                cuuint32_t box[2] = {128, 128};
+                cuuint32_t estr[2] = {1, 1};
+                const CUresult r = encode(&bt.tm[bt.count - 1], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                          const_cast<uint16_t*>(d.w), dims, strides, box, estr,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+            }
             bt.nblocks += blocks;
             if (bt.count == kMaxWeightBatch) {
                 cudaError_t e = flush();

@@ -37,7 +37,9 @@ def test_weight_c1_seeds(seed):
     _assert_weight_exact(synth.qwen3_weight(256, 256, seed))
 
 
-@pytest.mark.parametrize("n,k", [(300, 200), (129, 136), (1, 8), (128, 128), (131, 392), (640, 1024)])
+@pytest.mark.parametrize("n,k", [(300, 200), (129, 136), (1, 8), (128, 128), (131, 392), (640, 1024),
+                                 # k % 16 == 0: the bulk-staged path with ragged rows / columns
+                                 (300, 208), (129, 144), (1, 16), (200, 400), (1000, 1040)])
 def test_weight_ragged_shapes(n, k):
     _assert_weight_exact(synth.qwen3_weight(n, k, n * 7 + k))
 
@@ -186,3 +188,49 @@ def test_weight_batched_equals_individual():
     for (w, codes, scales), (oc, os_) in zip(items, refs):
         assert np.array_equal(to_host_u8(codes), oc)
         assert np.array_equal(to_host_f32(scales), os_)
+
+
+_BULK_SCRIPT = r"""
+import numpy as np, torch, oracle, synth
+from paper_2601_18150_b200 import fp8q
+from tests.helpers import to_dev_bf16, to_host_u8, to_host_f32
+shapes = [(300, 208), (129, 144), (1, 16), (200, 400), (1000, 1040), (128, 128), (640, 1024)]
+for i, (n, k) in enumerate(shapes):
+    bits = synth.qwen3_weight(n, k, 500 + i)
+    c, s = fp8q.quantize_weight_blockwise(to_dev_bf16(bits))
+    oc, os_ = oracle.quantize_weight_blockwise(bits)
+    assert np.array_equal(to_host_f32(s).view(np.uint32), os_.view(np.uint32)), (n, k, "scales")
+    assert np.array_equal(to_host_u8(c), oc), (n, k, "codes")
+bits = synth.uniform_bits((384, 512), 7)
+c, s = fp8q.quantize_weight_blockwise(to_dev_bf16(bits))
+oc, os_ = oracle.quantize_weight_blockwise(bits)
+assert np.array_equal(to_host_u8(c), oc) and np.array_equal(to_host_f32(s).view(np.uint32), os_.view(np.uint32))
+# a batch spanning several tensors: one bulk launch, ranges crossing tensor boundaries
+shapes = [(768, 512), (256, 384), (300, 208), (128, 1024)] * 5
+items, refs = [], []
+for i, (n, k) in enumerate(shapes):
+    bits = synth.qwen3_weight(n, k, seed=900 + i)
+    items.append((to_dev_bf16(bits), torch.empty((n, k), dtype=torch.uint8, device="cuda"),
+                  torch.empty(((n + 127) // 128, (k + 127) // 128), dtype=torch.float32, device="cuda")))
+    refs.append(oracle.quantize_weight_blockwise(bits))
+fp8q.quantize_weight_blockwise_batched(items)
+torch.cuda.synchronize()
+for (w, c, s), (oc, os_) in zip(items, refs):
+    assert np.array_equal(to_host_u8(c), oc) and np.array_equal(to_host_f32(s), os_)
+print("bulk ok")
+"""
+
+
+@pytest.mark.parametrize("path", ["bulk", "wide"])
+def test_weight_forced_path_ragged(path):
+    # The library picks the bulk-staged (TMA ring) or the block-strided kernel by batch size;
+    # force each on small ragged shapes (rows past n / columns past k, batches whose per-CTA
+    # block ranges cross tensor boundaries) in a fresh process (the override is read once).
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FP8Q_WEIGHT_KERNEL=path, PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _BULK_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "bulk ok" in r.stdout, r.stdout + r.stderr
