@@ -12,6 +12,14 @@
 // whatever the tile count, and the ring holds 6-11 k-blocks of weights in flight per SM.  A
 // range is walked as segments (its part of each tile); a tile covered by several CTAs is
 // finished by a deterministic fixup (below).
+// When whole tiles would leave at least half the SMs idle (qkv, o_proj, down_proj: 32-48
+// tiles), the kernel instead runs as CLUSTER split-K: a cluster of cs <= 8 CTAs per weight
+// tile, CTA rank r streaming k-blocks [r KB/cs, (r+1) KB/cs); each CTA parks its fp32 partial
+// in its own (by then idle) weight ring and, after one cluster barrier, sums a 1/cs slice of
+// the tile over the cluster's CTAs in rank order through distributed shared memory.  The
+// per-CTA timeline showed the stream-K fixup (fence, counter atomics, one dependent L2 round
+// trip per contributor, 64 KB of partials per contributor at M = 128) ending 5-12 us after the
+// last weight byte arrived; the DSMEM reduction replaces it with two cluster barriers.
 //
 // CTA = 12 warps (3 warpgroups):
 //   warp 0       TMA producer: per k-block W 128x128 B, X MTx128 B (rows >= m zero-filled by
@@ -35,6 +43,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -86,6 +95,7 @@ struct SkCfg {
     static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * (STAGE_BYTES + SA_SLOT) + 512;
     static_assert(MT % 16 == 0 && MT >= 16 && MT <= 128, "MMA N for M=128 must be a multiple of 16");
     static_assert(X_TILE % 1024 == 0, "X tile must be whole 128-byte-swizzle atoms");
+    static_assert(STAGES * W_TILE >= MT * SK_BN * 4, "cluster split-K parks its partial in the weight ring");
 };
 
 struct SkParams {
@@ -95,7 +105,10 @@ struct SkParams {
     int64_t ld_d;
     int out_f32;
     int m, n, num_kb, tiles;
-    int streamk;        // 1: ranges [c*T/G, (c+1)*T/G) per CTA; 0: whole tiles, strided
+    int streamk;        // 1: ranges [c*T/G, (c+1)*T/G) per CTA; 0: whole tiles, strided;
+                        // 2: cluster split-K -- cluster = one tile, CTA rank r its k-blocks
+                        //    [r*KB/cs, (r+1)*KB/cs), partials reduced through DSMEM
+    int cs;             // cluster size (mode 2)
     int64_t total;      // T = tiles * num_kb
     float* ws;          // stream-K partials: two [MT][128] fp32 slots per CTA
     int32_t* counters;  // [tiles], left zeroed
@@ -108,12 +121,13 @@ struct SkParams {
 __device__ __forceinline__ void sk_trace(const SkParams& p, uint32_t it, int ev) {
     if (p.trace != nullptr && blockIdx.x == 0 && it < 96) p.trace[it * 12 + ev] = static_cast<uint32_t>(clock64());
 }
-// every CTA's entry / exit on the global timer (ns): trace[1152 + 2 b + {0, 1}]
+// every CTA's events on the global timer (ns): trace[1152 + 4 b + which], which = 0 entry,
+// 1 exit, 2 first partial visible to the promotion warps, 3 last k-block promoted (pre-fixup)
 __device__ __forceinline__ void sk_trace_cta(const SkParams& p, int which) {
     if (p.trace != nullptr && blockIdx.x < 256) {
         uint64_t t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        p.trace[1152 + 2 * blockIdx.x + which] = static_cast<uint32_t>(t);
+        p.trace[1152 + 4 * blockIdx.x + which] = static_cast<uint32_t>(t);
     }
 }
 
@@ -124,14 +138,23 @@ struct SegIter {
     int64_t x, end;  // stream-K: position in [0, T) and this CTA's range end
     int t;           // tiled: next tile
     __device__ __forceinline__ void init(const SkParams& p) {
-        if (p.streamk) {
+        if (p.streamk == 1) {
             x = static_cast<int64_t>(blockIdx.x) * p.total / gridDim.x;
             end = static_cast<int64_t>(blockIdx.x + 1) * p.total / gridDim.x;
         }
         t = blockIdx.x;
     }
     __device__ __forceinline__ bool next(const SkParams& p, int& tile, int& kb0, int& kb1) {
-        if (p.streamk) {
+        if (p.streamk == 2) {  // one segment: rank r of cluster `tile`
+            if (t < 0) return false;
+            const int r = static_cast<int>(blockIdx.x) % p.cs;
+            tile = static_cast<int>(blockIdx.x) / p.cs;
+            kb0 = r * p.num_kb / p.cs;
+            kb1 = (r + 1) * p.num_kb / p.cs;
+            t = -1;
+            return true;
+        }
+        if (p.streamk == 1) {
             if (x >= end) return false;
             tile = static_cast<int>(x / p.num_kb);
             const int64_t t0 = int64_t(tile) * p.num_kb;
@@ -357,7 +380,10 @@ __global__ void __launch_bounds__(SK_THREADS, SkCfg<MT>::LIGHT ? 2 : 1)
                 const uint32_t buf = it % NBUF;
                 const uint32_t bph = (it / NBUF) & 1u;
                 mbar_wait(&tfull[buf], bph);
-                if (threadIdx.x == SK_EPI_WARP0 * 32) sk_trace(p, it, 2);
+                if (threadIdx.x == SK_EPI_WARP0 * 32) {
+                    sk_trace(p, it, 2);
+                    if (it == 0) sk_trace_cta(p, 2);
+                }
                 mbar_wait(&full[stage], ph);  // (already complete) orders the TMA-written scales
                 tc_fence_after();
                 const float* sa_s = smS + stage * SA_STRIDE + j0;
@@ -389,7 +415,13 @@ __global__ void __launch_bounds__(SK_THREADS, SkCfg<MT>::LIGHT ? 2 : 1)
                 if (threadIdx.x == SK_EPI_WARP0 * 32) sk_trace(p, it, 3);
             }
             const int64_t n_row = int64_t(tile) * SK_BN + r_in;
-            if (kb0 > 0 || kb1 < p.num_kb) {
+            if (p.streamk == 2) {
+                // cluster split-K: the partial goes to this CTA's (now idle) weight ring as
+                // red[j][row], reduced across the cluster after the cluster barrier below
+                float* red = reinterpret_cast<float*>(smW) + j0 * SK_BN + r_in;
+#pragma unroll
+                for (int j = 0; j < COLS; ++j) red[j * SK_BN] = acc[j];
+            } else if (kb0 > 0 || kb1 < p.num_kb) {
                 // partial tile (first or last segment of this CTA's range): park it, no wait
                 const int slot = si == 0 ? 0 : 1;
                 parked[slot] = tile;
@@ -403,6 +435,7 @@ __global__ void __launch_bounds__(SK_THREADS, SkCfg<MT>::LIGHT ? 2 : 1)
                 sk_store(p, n_row, j0, jn, acc);
             }
         }
+        if (threadIdx.x == SK_EPI_WARP0 * 32) sk_trace_cta(p, 3);
         // ---- stream-K fixup of the parked tiles (at most two per CTA): one fence, both
         // counters bumped in one round trip, then the sums of the tiles this CTA completes
         if (parked[0] >= 0 || parked[1] >= 0) {
@@ -433,18 +466,36 @@ __global__ void __launch_bounds__(SK_THREADS, SkCfg<MT>::LIGHT ? 2 : 1)
                 // CTA c parked tile t in slot 0 if t is the first tile of c's range, else slot 1.
                 // Unpredicated loads (columns past m hold stale values that are never stored)
                 // so each CTA's whole row segment is in flight at once.
+                // The contributors' partials are fetched FC CTAs at a time (all loads of a group in
+                // flight together: one L2 round trip per group, not one per contributing CTA --
+                // the per-CTA timeline showed the fixup CTAs exiting ~8 us after their stream
+                // ended with one dependent round trip per contributor) and summed in CTA order,
+                // so the result is bit-identical to the one-at-a-time sum.
+                constexpr int FC_REGS = C::LIGHT ? 32 : 64;  // light: 80 registers per thread in all
+                constexpr int FC = COLS >= FC_REGS ? 1 : FC_REGS / COLS;
                 float acc[COLS];
 #pragma unroll
                 for (int j = 0; j < COLS; ++j) acc[j] = 0.0f;
 #pragma unroll 1
-                for (int c = c_first; c <= c_last; ++c) {
-                    const int64_t c_start = int64_t(c) * p.total / gridDim.x;
-                    const float* src = p.ws + (int64_t(2 * c + (c_start < t0 ? 1 : 0)) * MT + j0) * SK_BN + r_in;
-                    float v[COLS];
+                for (int cg = c_first; cg <= c_last; cg += FC) {
+                    float v[FC][COLS];
 #pragma unroll
-                    for (int j = 0; j < COLS; ++j) v[j] = __ldcg(src + j * SK_BN);
+                    for (int f = 0; f < FC; ++f) {
+                        const int c = cg + f;
+                        if (FC == 1 || c <= c_last) {
+                            const int64_t c_start = int64_t(c) * p.total / gridDim.x;
+                            const float* src =
+                                p.ws + (int64_t(2 * c + (c_start < t0 ? 1 : 0)) * MT + j0) * SK_BN + r_in;
 #pragma unroll
-                    for (int j = 0; j < COLS; ++j) acc[j] += v[j];
+                            for (int j = 0; j < COLS; ++j) v[f][j] = __ldcg(src + j * SK_BN);
+                        }
+                    }
+#pragma unroll
+                    for (int f = 0; f < FC; ++f)
+                        if (FC == 1 || cg + f <= c_last) {
+#pragma unroll
+                            for (int j = 0; j < COLS; ++j) acc[j] += v[f][j];
+                        }
                 }
                 if (threadIdx.x == SK_EPI_WARP0 * 32) p.counters[t] = 0;  // reusable workspace
                 const int64_t n_row = int64_t(t) * SK_BN + r_in;
@@ -455,6 +506,71 @@ __global__ void __launch_bounds__(SK_THREADS, SkCfg<MT>::LIGHT ? 2 : 1)
 
     tc_fence_before();
     __syncthreads();
+    if (p.streamk == 2) {
+        // ---- cluster split-K reduction: every CTA of the cluster parked its [MT][128] fp32
+        // partial in its own shared memory; CTA r sums elements [r E/cs, (r+1) E/cs) of the
+        // E = m x 128 live ones over the cluster's CTAs IN RANK ORDER (deterministic), reading
+        // the peers' shared memory through DSMEM, and stores them.  No global workspace, no
+        // fences, no atomics.
+        cluster_sync_all();
+        if (warp >= SK_EPI_WARP0) {  // the promotion warps (216 registers; warps 0-3 hold 72)
+            grid_dependency_wait();
+            const uint32_t rank = cluster_ctarank();
+            const int tile = static_cast<int>(blockIdx.x) / p.cs;
+            // units of 4 consecutive weight rows of one token column: one 16-byte DSMEM load per
+            // peer (scalar remote loads were measured at ~4 B/cycle: 6 us for a 128 x 128 tile)
+            const int U = p.m * (SK_BN / 4);
+            const int u1 = static_cast<int>((int64_t(rank) + 1) * U / p.cs);
+            const uint32_t red0 = smem_u32(smW);
+            const int te = threadIdx.x - SK_EPI_WARP0 * 32;
+            constexpr int RU = 1;  // units per thread per pass (all cs loads of a unit in flight together)
+            for (int q0 = static_cast<int>(int64_t(rank) * U / p.cs) + te; q0 < u1; q0 += RU * SK_EPI_WARPS * 32) {
+                float4 v[RU][8];
+#pragma unroll
+                for (int r = 0; r < RU; ++r) {
+                    const int q = q0 + r * SK_EPI_WARPS * 32;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        if (c < p.cs && q < u1) {
+                            uint32_t ra;
+                            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(red0 + 16u * q), "r"(c));
+                            asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                         : "=f"(v[r][c].x), "=f"(v[r][c].y), "=f"(v[r][c].z), "=f"(v[r][c].w)
+                                         : "r"(ra));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < RU; ++r) {
+                    const int q = q0 + r * SK_EPI_WARPS * 32;
+                    if (q >= u1) break;
+                    float4 sum = v[r][0];
+#pragma unroll
+                    for (int c = 1; c < 8; ++c)
+                        if (c < p.cs) {
+                            sum.x += v[r][c].x;
+                            sum.y += v[r][c].y;
+                            sum.z += v[r][c].z;
+                            sum.w += v[r][c].w;
+                        }
+                    const int j = q / (SK_BN / 4), row = 4 * (q - j * (SK_BN / 4));
+                    const int64_t n_row = int64_t(tile) * SK_BN + row;
+                    const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        if (n_row + t < p.n) {
+                            if (p.out_f32)
+                                static_cast<float*>(p.d)[int64_t(j) * p.ld_d + n_row + t] = sv[t];
+                            else
+                                static_cast<__nv_bfloat16*>(p.d)[int64_t(j) * p.ld_d + n_row + t] =
+                                    __float2bfloat16_rn(sv[t]);
+                        }
+                    }
+                }
+            }
+        }
+        cluster_sync_all();  // no CTA leaves while a peer may still read its shared memory
+    }
     if (threadIdx.x == 0) {
         sk_trace(p, 0, 6);
         sk_trace_cta(p, 1);
@@ -516,6 +632,50 @@ cudaError_t sk_device_info(int& sms) {
     return cudaSuccess;
 }
 
+// Cluster split-K (mode 2) applies when whole weight tiles would leave at least half the SMs
+// idle: the largest cs <= 8 with tiles * cs <= sms whose clusters are all co-resident
+// (cudaOccupancyMaxActiveClusters: a cluster must fit in one GPC).  0: not applicable.
+// Dev override FP8Q_SKINNY_CLUSTER=0 disables it (stream-K instead).  Cached per shape class.
+template <int MT>
+int sk_cluster_size(int tiles, int num_kb, int sms) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("FP8Q_SKINNY_CLUSTER");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    if (!enabled || tiles * 2 > sms || num_kb < 4) return 0;
+    struct Entry { int tiles, num_kb, sms, cs; };
+    static Entry cache[32];
+    static int used = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < used; ++i)
+        if (cache[i].tiles == tiles && cache[i].num_kb == num_kb && cache[i].sms == sms) return cache[i].cs;
+    int c = std::min(8, std::min(sms / tiles, num_kb / 2));
+    for (; c >= 2; --c) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(static_cast<unsigned>(tiles * c));
+        q.blockDim = dim3(SK_THREADS);
+        q.dynamicSmemBytes = SkCfg<MT>::SMEM_BYTES;
+        cudaLaunchAttribute ca;
+        ca.id = cudaLaunchAttributeClusterDimension;
+        ca.val.clusterDim.x = static_cast<unsigned>(c);
+        ca.val.clusterDim.y = 1;
+        ca.val.clusterDim.z = 1;
+        q.attrs = &ca;
+        q.numAttrs = 1;
+        int active = 0;
+        const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, fp8_gemm_skinny_kernel<MT>, &q);
+        if (std::getenv("FP8Q_DEBUG_CLUSTER") != nullptr)
+            std::fprintf(stderr, "[fp8q] skinny MT=%d tiles=%d kb=%d: cluster %d -> %d active (%s)\n", MT, tiles,
+                         num_kb, c, active, cudaGetErrorString(e));
+        if (e == cudaSuccess && active >= tiles) break;
+        cudaGetLastError();
+    }
+    const int cs = c >= 2 ? c : 0;
+    if (used < 32) cache[used++] = Entry{tiles, num_kb, sms, cs};
+    return cs;
+}
+
 template <int MT>
 cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encode, int sms, cudaStream_t stream) {
     CUtensorMap tmW, tmX, tmS;
@@ -562,6 +722,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     p.tiles = static_cast<int>((a.n + SK_BN - 1) / SK_BN);
     p.total = int64_t(p.tiles) * p.num_kb;
     p.streamk = 0;
+    p.cs = 1;
     p.ws = nullptr;
     p.counters = nullptr;
     p.trace = get_gemm_trace();
@@ -573,16 +734,26 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
         p.ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + SK_COUNTER_BYTES);
         grid = static_cast<unsigned>(sk_grid(p.tiles, p.num_kb, sms));
     }
+    const int cs = sk_cluster_size<MT>(p.tiles, p.num_kb, sms);
+    if (cs >= 2) {
+        p.streamk = 2;
+        p.cs = cs;
+        grid = static_cast<unsigned>(p.tiles * cs);
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(SK_THREADS);
     cfg.dynamicSmemBytes = SkCfg<MT>::SMEM_BYTES;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = static_cast<unsigned>(p.cs);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT>, tmW, tmX, tmS, p);
 }
 

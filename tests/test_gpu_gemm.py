@@ -237,6 +237,8 @@ def test_splitk_workspace_reused_across_shapes():
 @pytest.mark.parametrize("m,n,k", [
     (1, 256, 128), (3, 200, 256), (16, 1000, 512), (17, 384, 1024), (33, 4096, 4096),
     (64, 6144, 4096), (100, 1032, 1536), (127, 512, 12288), (128, 4096, 4096),
+    # cluster split-K sizes 7, 4 (ragged last tile), 4 (148 CTAs) and 2
+    (5, 128 * 21, 2048), (40, 128 * 29 + 64, 1024), (2, 128 * 37, 4096), (9, 128 * 74, 512),
 ])
 def test_skinny_decode_vs_oracle(m, n, k):
     # 1 <= m <= 128 (dense) runs gemm_skinny.cu: tokens in the MMA N dimension (16..128 padded
@@ -278,3 +280,31 @@ def test_skinny_matches_tile_kernel_when_scales_misaligned(m, with_ws):
         torch.cuda.synchronize()
         assert st == 0
         assert rel_frobenius(yt.cpu().numpy(), y.cpu().numpy()) <= 1e-6
+
+
+_STREAMK_SCRIPT = r"""
+import numpy as np, torch, oracle
+from tests.test_gpu_gemm import _operands, _run
+from tests.helpers import rel_frobenius
+for i, (m, n, k) in enumerate([(1, 6144, 4096), (64, 4096, 4096), (17, 384, 1024), (128, 4096, 12288)]):
+    a, sa, b, sb = _operands(m, n, k, 70 + i)
+    y = _run(a, sa, b, sb)
+    rows = np.arange(min(m, 8))
+    assert rel_frobenius(y[:len(rows)].cpu().numpy(), oracle.gemm_rows(a, sa, b, sb, rows)) <= 1e-5, (m, n, k)
+    assert torch.equal(_run(a, sa, b, sb).view(torch.int32), y.view(torch.int32))
+print("streamk ok")
+"""
+
+
+def test_skinny_streamk_path_when_cluster_split_disabled():
+    # Shapes with few weight tiles run the cluster split-K mode (DSMEM reduction); with it
+    # disabled (dev override, read once per process) the same shapes take the stream-K path
+    # (global-workspace fixup), which must stay correct and deterministic.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FP8Q_SKINNY_CLUSTER="0", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _STREAMK_SCRIPT], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "streamk ok" in r.stdout, r.stdout + r.stderr

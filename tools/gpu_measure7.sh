@@ -1,0 +1,10 @@
+# dev: cluster-size choice per shape, reduction ILP, decode graph timing
+mkdir -p gpurun_out
+
+
+timeout 900 python -m pytest tests/test_gpu_gemm.py -x -q -k skinny > gpurun_out/gemm_parity.log 2>&1; echo parity=$?
+tail -2 gpurun_out/gemm_parity.log
+for mnk in "1 6144 4096" "64 6144 4096" "128 4096 4096"; do
+echo "== trace $mnk"; timeout 120 python tools/skinny_trace.py $mnk 2>&1 | head -4
+done
+echo "== decode cluster"; timeout 600 python tools/kernel_bench.py --what none --decode --graph --flush read

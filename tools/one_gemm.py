@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Launch one kernel shape a few times (target for `ncu -k regex:... -s W -c N`).
-usage: one_gemm.py gemm M N K | wq N K | aq M K | rms M K | silu M I | kv T cols | mxgemm M N K | grouped T name [skew]"""
+usage: one_gemm.py gemm M N K | wq N K | wqlayer | aq M K | rms M K | silu M I | kv T cols | mxgemm M N K | grouped T name [skew]"""
 import os
 import sys
 
@@ -29,6 +29,14 @@ elif what == "wq":
     w = (torch.randn((n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
     for _ in range(reps):
         fp8q.quantize_weight_blockwise(w)
+elif what == "wqlayer":  # one Qwen3-8B layer's 4 weights in one batched launch (the sync step)
+    items = []
+    for n, k in synth.QWEN3_8B_LINEARS.values():
+        w = (torch.randn((n, k), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+        items.append((w, torch.empty((n, k), dtype=torch.uint8, device=dev),
+                      torch.empty(((n + 127) // 128, (k + 127) // 128), dtype=torch.float32, device=dev)))
+    for _ in range(reps):
+        fp8q.quantize_weight_blockwise_batched(items)
 elif what == "aq":
     m, k = map(int, sys.argv[2:4])
     x = torch.randn((m, k), generator=g, device=dev).to(torch.bfloat16)

@@ -22,7 +22,7 @@ wq, ws = fp8q.quantize_weight_blockwise(w)
 xq, xs = fp8q.quantize_act_per_token_group(x)
 lib = fp8q.load_library()
 lib.fp8q_debug_set_gemm_trace.argtypes = [ctypes.c_void_p]
-tr = torch.zeros(96 * 12 + 512, dtype=torch.int32, device=dev)
+tr = torch.zeros(96 * 12 + 1024, dtype=torch.int32, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 for _ in range(3):
     fp8q.fp8_block_gemm(xq, xs, wq, ws)
@@ -37,13 +37,19 @@ torch.cuda.synchronize()
 lib.fp8q_debug_set_gemm_trace(None)
 allt = tr.cpu().numpy().view(np.uint32).astype(np.int64)
 t = allt[:1152].reshape(96, 12)
-cta = allt[1152:].reshape(256, 2)
+cta = allt[1152:].reshape(256, 4)
 live = np.nonzero(cta[:, 1])[0]
 t0 = cta[live, 0].min()
 ent, ext = (cta[live, 0] - t0) % (1 << 32), (cta[live, 1] - t0) % (1 << 32)
 print(f"CTAs {len(live)}: entry ns min/med/max {ent.min()}/{int(np.median(ent))}/{ent.max()}  "
       f"exit ns min/med/max {ext.min()}/{int(np.median(ext))}/{ext.max()}")
 print("exit histogram (us):", np.histogram(ext / 1000, bins=8)[0].tolist(), np.round(np.histogram(ext / 1000, bins=8)[1], 1).tolist())
+first, sdone = (cta[live, 2] - t0) % (1 << 32), (cta[live, 3] - t0) % (1 << 32)
+print(f"first partial ns min/med/max {first.min()}/{int(np.median(first))}/{first.max()}  "
+      f"stream done ns min/med/max {sdone.min()}/{int(np.median(sdone))}/{sdone.max()}")
+slow = np.argsort(ext)[-6:]
+for i in slow:
+    print(f"  slow CTA {live[i]:3d}: entry {ent[i]} first {first[i]} stream_done {sdone[i]} exit {ext[i]}")
 base = t[0, 4]
 rel = (t - base) % (1 << 32)
 print(f"entry 0  setup_done {rel[0, 5]}  dependency_wait_done {rel[0, 7]}  exit {rel[0, 6]}")
