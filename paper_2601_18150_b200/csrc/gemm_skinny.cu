@@ -93,9 +93,10 @@ struct SkCfg {
     static constexpr int COLS = MT / 2;  // token columns per promotion thread
     static constexpr uint32_t IDESC = idesc_e4m3_f32(SK_BN, MT);
     static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * (STAGE_BYTES + SA_SLOT) + 512;
-    static_assert(MT % 16 == 0 && MT >= 16 && MT <= 128, "MMA N for M=128 must be a multiple of 16");
+    static_assert(MT % 16 == 0 && MT >= 16 && MT <= 256, "MMA N for M=128 must be a multiple of 16, <= 256");
     static_assert(X_TILE % 1024 == 0, "X tile must be whole 128-byte-swizzle atoms");
-    static_assert(STAGES * W_TILE >= MT * SK_BN * 4, "cluster split-K parks its partial in the weight ring");
+    // cluster split-K parks its partial in the (contiguous) W and X rings
+    static_assert(STAGES * (W_TILE + X_TILE) >= MT * SK_BN * 4, "no room for the cluster split-K partial");
 };
 
 struct SkParams {
@@ -582,7 +583,7 @@ __global__ void __launch_bounds__(SK_THREADS, SkCfg<MT>::LIGHT ? 2 : 1)
 }
 
 // ------------------------------------------------------------------------------ host side
-int sk_mt(int64_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : 128; }
+int sk_mt(int64_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 256; }
 
 // Stream-K grid: one CTA per SM, but at least 2 k-blocks per CTA.
 int64_t sk_grid(int64_t tiles, int64_t num_kb, int sms) {
@@ -595,7 +596,7 @@ bool sk_streamk_possible(int64_t n, int64_t k, int sms) {
     return tiles * 4 <= static_cast<int64_t>(SK_COUNTER_BYTES) && sk_grid(tiles, k / SK_BK, sms) > 1;
 }
 size_t sk_ws_bytes(int64_t m, int64_t n, int64_t k, int sms) {
-    if (!sk_streamk_possible(n, k, sms)) return 0;
+    if (m > 128 || !sk_streamk_possible(n, k, sms)) return 0;  // M > 128: cluster split-K only
     const int64_t tiles = (n + SK_BN - 1) / SK_BN;
     return SK_COUNTER_BYTES + static_cast<size_t>(2 * sk_grid(tiles, k / SK_BK, sms)) * sk_mt(m) * SK_BN * 4;
 }
@@ -625,6 +626,7 @@ cudaError_t sk_device_info(int& sms) {
         SK_ATTR(32)
         SK_ATTR(64)
         SK_ATTR(128)
+        SK_ATTR(256)
 #undef SK_ATTR
         di.attr_set = true;
     }
@@ -771,6 +773,12 @@ bool skinny_gemm_applies(const GemmArgs& a) {
     // Measured (tools/kernel_bench.py --decode --graph, Qwen3-8B shapes): up to M = 32 this
     // kernel wins everywhere; above, the 128 x 256 tile kernel wins once it has >= 64 tiles to
     // spread (gate_up), this one where the tile kernel would leave most SMs idle (qkv, o, down).
+    if (a.m > 128) {  // M = 129..256: only as cluster split-K (few weight tiles, e.g. o/down/qkv)
+        if (forced == 16) return true;
+        int sms = 0;
+        if (sk_device_info(sms) != cudaSuccess) return false;
+        return sk_cluster_size<256>(static_cast<int>((a.n + SK_BN - 1) / SK_BN), static_cast<int>(a.k / SK_BK), sms) >= 2;
+    }
     return forced == 16 || a.m <= 32 || (a.n + 255) / 256 < 64;
 }
 
@@ -790,7 +798,8 @@ cudaError_t launch_fp8_gemm_skinny(const GemmArgs& a, void* encode_fn, cudaStrea
         case 16: return sk_launch<16>(a, encode, sms, stream);
         case 32: return sk_launch<32>(a, encode, sms, stream);
         case 64: return sk_launch<64>(a, encode, sms, stream);
-        default: return sk_launch<128>(a, encode, sms, stream);
+        case 128: return sk_launch<128>(a, encode, sms, stream);
+        default: return sk_launch<256>(a, encode, sms, stream);
     }
 }
 

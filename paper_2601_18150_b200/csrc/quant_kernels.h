@@ -53,8 +53,9 @@ struct GemmArgs {
     size_t workspace_bytes;
 };
 
-// Decode-sized dense GEMMs (1 <= m <= kSkinnyMaxM) run the swap-AB kernel of gemm_skinny.cu.
-constexpr int kSkinnyMaxM = 128;
+// Decode-sized dense GEMMs (1 <= m <= kSkinnyMaxM) run the swap-AB kernel of gemm_skinny.cu
+// (m > 128 only where its cluster split-K mode applies).
+constexpr int kSkinnyMaxM = 256;
 bool skinny_gemm_applies(const GemmArgs& a);
 size_t skinny_workspace_bytes(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_fp8_gemm_skinny(const GemmArgs& a, void* encode_fn, cudaStream_t stream);

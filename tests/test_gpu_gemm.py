@@ -239,6 +239,8 @@ def test_splitk_workspace_reused_across_shapes():
     (64, 6144, 4096), (100, 1032, 1536), (127, 512, 12288), (128, 4096, 4096),
     # cluster split-K sizes 7, 4 (ragged last tile), 4 (148 CTAs) and 2
     (5, 128 * 21, 2048), (40, 128 * 29 + 64, 1024), (2, 128 * 37, 4096), (9, 128 * 74, 512),
+    # M = 129..256: the swap-AB kernel with 256 token columns, cluster split-K only
+    (200, 4096, 4096), (256, 1000, 2048), (129, 6144, 1024),
 ])
 def test_skinny_decode_vs_oracle(m, n, k):
     # 1 <= m <= 128 (dense) runs gemm_skinny.cu: tokens in the MMA N dimension (16..128 padded
