@@ -543,7 +543,7 @@ def run_sync(args):
                       "local_requant_gbs": round(local_elems * WEIGHT_BYTES_PER_ELEM / (ms * 1e-3) / 1e9, 1)},
         "roofline": {"bound": "hbm" if world == 1 else "nvlink", "achieved": round(gbs / world, 1) if world == 1 else None,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4) if world == 1 else None,
-                     "traffic": None, "kernel": "weight_blockwise_wide_kernel (batched, 16 tensors per launch)"},
+                     "traffic": None, "kernel": "weight_blockwise_bulk_kernel (TMA-staged; batched, 16 tensors per launch)"},
         "gpu_launches": int(launches), "clocks": clk,
     }
     if rank == 0:

@@ -114,6 +114,21 @@ def test_nonfinite_flag():
     x[2, 17] = 0xFFC0  # NaN
     fp8q.quantize_act_per_token_group(to_dev_bf16(x), nonfinite_flag=flag)
     assert int(flag.item()) == 1
+    # every non-finite kind on both quantizers' production paths (NaN payloads, -Inf, a NaN
+    # next to the block's finite amax), on shapes that take the wide / staged kernels
+    for n, k in [(256, 256), (12288, 4096)]:
+        for pos, val in [((5, 9), 0x7FC1), ((n - 1, k - 1), 0xFF80), ((130, 129), 0xFFFF)]:
+            flag.zero_()
+            w = synth.qwen3_weight(n, k, 1)
+            w[pos] = val
+            fp8q.quantize_weight_blockwise(to_dev_bf16(w), nonfinite_flag=flag)
+            assert int(flag.item()) == 1, (n, k, pos, hex(val))
+            flag.zero_()
+            fp8q.quantize_act_per_token_group(to_dev_bf16(w), nonfinite_flag=flag)
+            assert int(flag.item()) == 1, (n, k, pos, hex(val))
+    flag.zero_()
+    fp8q.quantize_weight_blockwise(to_dev_bf16(synth.qwen3_weight(4096, 4096, 1)), nonfinite_flag=flag)
+    assert int(flag.item()) == 0
 
 
 # ------------------------------------------------------------------------------ activations
