@@ -73,7 +73,7 @@ constexpr int pow2_at_least(int v, int lo) {
     return p;
 }
 
-template <int MT>
+template <int MT, bool L = (MT <= 32)>
 struct SkCfg {
     static constexpr int W_TILE = SK_BN * SK_BK;   // 16 KB
     static constexpr int X_TILE = MT * SK_BK;      // MT x 128 B (a multiple of 1024 B: SW128 atoms)
@@ -83,7 +83,7 @@ struct SkCfg {
     // MT <= 32: half the smem, registers and TMEM, so two CTAs -- this GEMM's and the next
     // one's (programmatic dependent launch) -- fit on an SM and the next GEMM's weight stream
     // starts while this one drains
-    static constexpr bool LIGHT = MT <= 32;
+    static constexpr bool LIGHT = L;
     static constexpr int BUDGET = LIGHT ? SK_SMEM_BUDGET / 2 : SK_SMEM_BUDGET;
     static constexpr int STAGES_RAW = BUDGET / (STAGE_BYTES + SA_SLOT);
     static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
@@ -226,11 +226,11 @@ __device__ __forceinline__ void sk_store(const SkParams& p, int64_t n_row, int j
     }
 }
 
-template <int MT>
-__global__ void __launch_bounds__(SK_THREADS, SkCfg<MT>::LIGHT ? 2 : 1)
+template <int MT, bool L>
+__global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
     fp8_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                            const __grid_constant__ CUtensorMap tmS, const SkParams p) {
-    using C = SkCfg<MT>;
+    using C = SkCfg<MT, L>;
     constexpr int STAGES = C::STAGES;
     constexpr int NBUF = C::NBUF;
     constexpr int COLS = C::COLS;
@@ -618,15 +618,17 @@ cudaError_t sk_device_info(int& sms) {
     if (!di.attr_set) {
         e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return e;
-#define SK_ATTR(MT)                                                                                      \
-    e = cudaFuncSetAttribute(fp8_gemm_skinny_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                             static_cast<int>(SkCfg<MT>::SMEM_BYTES));                                 \
+#define SK_ATTR(MT, L)                                                                                  \
+    e = cudaFuncSetAttribute(fp8_gemm_skinny_kernel<MT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             static_cast<int>(SkCfg<MT, L>::SMEM_BYTES));                                \
     if (e != cudaSuccess) return e;
-        SK_ATTR(16)
-        SK_ATTR(32)
-        SK_ATTR(64)
-        SK_ATTR(128)
-        SK_ATTR(256)
+        SK_ATTR(16, true)
+        SK_ATTR(16, false)
+        SK_ATTR(32, true)
+        SK_ATTR(32, false)
+        SK_ATTR(64, false)
+        SK_ATTR(128, false)
+        SK_ATTR(256, false)
 #undef SK_ATTR
         di.attr_set = true;
     }
@@ -657,7 +659,7 @@ int sk_cluster_size(int tiles, int num_kb, int sms) {
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3(static_cast<unsigned>(tiles * c));
         q.blockDim = dim3(SK_THREADS);
-        q.dynamicSmemBytes = SkCfg<MT>::SMEM_BYTES;
+        q.dynamicSmemBytes = SkCfg<MT, false>::SMEM_BYTES;
         cudaLaunchAttribute ca;
         ca.id = cudaLaunchAttributeClusterDimension;
         ca.val.clusterDim.x = static_cast<unsigned>(c);
@@ -666,7 +668,7 @@ int sk_cluster_size(int tiles, int num_kb, int sms) {
         q.attrs = &ca;
         q.numAttrs = 1;
         int active = 0;
-        const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, fp8_gemm_skinny_kernel<MT>, &q);
+        const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, fp8_gemm_skinny_kernel<MT, false>, &q);
         if (std::getenv("FP8Q_DEBUG_CLUSTER") != nullptr)
             std::fprintf(stderr, "[fp8q] skinny MT=%d tiles=%d kb=%d: cluster %d -> %d active (%s)\n", MT, tiles,
                          num_kb, c, active, cudaGetErrorString(e));
@@ -745,7 +747,16 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(SK_THREADS);
-    cfg.dynamicSmemBytes = SkCfg<MT>::SMEM_BYTES;
+    // M <= 32 keeps the half-budget config (two CTAs per SM, so the next GEMM's CTAs start under
+    // PDL while this one drains) in every mode; FP8Q_SKINNY_HEAVY_CLUSTER=1 (dev A/B) runs the
+    // cluster mode with the full ring instead: measured qkv 11.6 -> 10.9 us but o_proj 7.9 -> 8.5
+    // us per GEMM (graph, M = 1), i.e. no net gain.
+    static const bool heavy_cluster = [] {
+        const char* e = std::getenv("FP8Q_SKINNY_HEAVY_CLUSTER");
+        return e != nullptr && e[0] == '1';
+    }();
+    const bool light = MT <= 32 && !(p.streamk == 2 && heavy_cluster);
+    cfg.dynamicSmemBytes = light ? SkCfg<MT, MT <= 32>::SMEM_BYTES : SkCfg<MT, false>::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -756,7 +767,8 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT>, tmW, tmX, tmS, p);
+    if (light) return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, MT <= 32>, tmW, tmX, tmS, p);
+    return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, false>, tmW, tmX, tmS, p);
 }
 
 }  // namespace
