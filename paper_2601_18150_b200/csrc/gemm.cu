@@ -845,8 +845,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 mbar_wait(&tempty[i % NBUF], (i / NBUF) & 1u);
             }
         }
-    } else if ((warp == 2 || warp == 3) && !p.out_f32) {
+    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128) {
         // ------------------------------------------------------------ store warps (BF16)
+        // (only where promote_tile parks BF16 slices for them: 128 columns per half; with
+        // PBN = 128 the promotion warps store their tile themselves -- gating on out_f32 alone
+        // left these warps waiting for slices that never come, a hang of dev kind 1128)
         const int h = warp - 2;
         TileCursor<2 * BM, PAIR_RASTER_GM> cur;
         cur.init(p);
