@@ -97,7 +97,9 @@ struct KParams {
     int32_t* counters;       // split-K arrival counters [tile], zero between launches
     uint32_t* trace;         // dev-only timeline (fp8q_debug_set_trace), nullptr in production
     int debug_mode;          // dev-only: 1 = promotion skips TMEM loads + FMAs (MMA pipe ceiling),
-                             // 2 = also no TMA after the first stages (tensor-core-only ceiling)
+                             // 2 = also no TMA after the first stages (tensor-core-only ceiling),
+                             // 3 = (pair) the MMA issuer ignores TMEM buffer releases and the
+                             //     promotion/store warps idle: TMA + MMA without the release chain
     int groups;
 };
 
@@ -735,7 +737,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);                  // multicast commit
-            // leader: the promotion warps of both CTAs (SPLIT: of one column half)
+            // leader: the promotion warps of both CTAs (SPLIT: of one column half).  (Funnelling the
+            // peer's 8 releases through one forwarded remote arrive was measured: no change.)
             mbar_init(&tempty[b], SPLIT ? NUM_EPI_WARPS : 2 * NUM_EPI_WARPS);
         }
         for (int hh = 0; hh < 2; ++hh) {
@@ -767,6 +770,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
+                    if (p.debug_mode == 2 && it >= STAGES) continue;  // dev: operands stay resident
                     mbar_wait(&empty[stage], ph ^ 1u);
                     trace_ev(p, it, 0);
                     if (leader)
@@ -822,9 +826,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     }
                     const uint32_t buf = it % NBUF;
                     const uint32_t bph = (it / NBUF) & 1u;
-                    mbar_wait(&tempty[buf], bph ^ 1u);
+                    if (p.debug_mode != 3) mbar_wait(&tempty[buf], bph ^ 1u);  // dev 3: no release chain
                     trace_ev(p, it, 1);
-                    mbar_wait(&full[stage], ph);
+                    if (p.debug_mode != 2 || it < STAGES) mbar_wait(&full[stage], ph);  // dev 2: no TMA
                     trace_ev(p, it, 2);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(smA + stage * A_TILE);
@@ -840,12 +844,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
             // the peer's last remote arrivals must land before the barriers go away
             const uint32_t slots = SPLIT ? 2u * it : it;
-            for (uint32_t j = 0; j < NBUF && j < slots; ++j) {
+            if (p.debug_mode == 3 && slots > 0) {  // dev 3: nobody releases; wait for the last MMAs
+                mbar_wait(&tfull[(slots - 1) % NBUF], ((slots - 1) / NBUF) & 1u);
+            }
+            for (uint32_t j = 0; j < NBUF && j < slots && p.debug_mode != 3; ++j) {
                 const uint32_t i = slots - 1 - j;
                 mbar_wait(&tempty[i % NBUF], (i / NBUF) & 1u);
             }
         }
-    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128) {
+    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128 && p.debug_mode != 3) {
         // ------------------------------------------------------------ store warps (BF16)
         // (only where promote_tile parks BF16 slices for them: 128 columns per half; with
         // PBN = 128 the promotion warps store their tile themselves -- gating on out_f32 alone
@@ -861,7 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             store_tile_half(p, smEpi, h, lane, cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM,
                             int64_t(cur.row0) + cur.rows, col0, stg_full, stg_empty, tile_no);
         }
-    } else if (warp >= EPI_WARP0) {
+    } else if (warp >= EPI_WARP0 && p.debug_mode != 3) {  // dev 3: promotion warps idle
         // ---------------------------------------------------------------- promotion warps
         regs_inc<REGS_EPI>();
         const int h = (warp - EPI_WARP0) >> 2;
