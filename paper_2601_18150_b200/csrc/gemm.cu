@@ -278,7 +278,9 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
         tc_fence_after();
         const bool tr = (threadIdx.x == EPI_WARP0 * 32);
         if (tr) trace_ev(p, it, 3);
+        const bool tr_last = (threadIdx.x == (EPI_WARP0 + NUM_EPI_WARPS - 1) * 32);
         if (p.debug_mode >= 1) {
+            if (tr_last) trace_ev(p, it, 9);  // dev: the last promotion warp sees the partial
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -287,6 +289,8 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
                 else
                     mbar_arrive(&tempty[buf]);
             }
+            if (tr) trace_ev(p, it, 8);        // dev: first warp released
+            if (tr_last) trace_ev(p, it, 10);  // dev: last warp released
             continue;
         }
         const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) +
@@ -587,6 +591,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t ph = (it / STAGES) & 1u;
                     const uint32_t buf = it % NBUF;
                     const uint32_t bph = (it / NBUF) & 1u;
+                    trace_ev(p, it, 11);  // dev: issuer starts waiting for the buffer
                     mbar_wait(&tempty[buf], bph ^ 1u);  // promotion warps drained this buffer
                     trace_ev(p, it, 1);
                     if (p.debug_mode != 2 || it < STAGES) mbar_wait(&full[stage], ph);  // TMA landed A and B
@@ -826,6 +831,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     }
                     const uint32_t buf = it % NBUF;
                     const uint32_t bph = (it / NBUF) & 1u;
+                    trace_ev(p, it, 11);  // dev: issuer starts waiting for the buffer
                     if (p.debug_mode != 3) mbar_wait(&tempty[buf], bph ^ 1u);  // dev 3: no release chain
                     trace_ev(p, it, 1);
                     if (p.debug_mode != 2 || it < STAGES) mbar_wait(&full[stage], ph);  // dev 2: no TMA

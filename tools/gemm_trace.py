@@ -41,3 +41,12 @@ for i in range(96):
     prev = row[2]
     print(f"{i:3d} " + " ".join(f"{v:10d}" for v in row)
           + f"  {d_issue:8d} {row[3] - row[2]:8d} {row[4] - row[3]:8d} {row[5] - row[3]:8d}")
+
+if os.environ.get("FP8Q_GEMM_DEBUG", "0") == "1":
+    # release path (dev mode 1): 3 first warp sees partial, 9 last warp sees it, 8/10 first/last
+    # warp released, 11 issuer starts waiting for the buffer of k-block i, 1 issuer sees it free
+    print("kb  ready_w0 ready_wlast  rel_w0 rel_wlast  mma_prewait(i+2)  tfree(i+2)   [relative to ready_w0]")
+    for i in range(8, 20):
+        r = t[i]
+        n2 = t[i + 2]
+        print(f"{i:3d} {0:8d} {r[9] - r[3]:11d} {r[8] - r[3]:8d} {r[10] - r[3]:9d} {n2[11] - r[3]:17d} {n2[1] - r[3]:11d}")
