@@ -99,7 +99,8 @@ struct KParams {
     int debug_mode;          // dev-only: 1 = promotion skips TMEM loads + FMAs (MMA pipe ceiling),
                              // 2 = also no TMA after the first stages (tensor-core-only ceiling),
                              // 3 = (pair) the MMA issuer ignores TMEM buffer releases and the
-                             //     promotion/store warps idle: TMA + MMA without the release chain
+                             //     promotion/store warps idle: TMA + MMA without the release chain,
+                             // 4 = promotion reads TMEM (all chunks) but does no FMAs
     int groups;
 };
 
@@ -295,6 +296,24 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
         }
         const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) +
                                (SPLIT ? buf * EPI_COLS : buf * BN + h * EPI_COLS);
+        if (p.debug_mode == 4) {  // dev: the TMEM read-out alone (no FMAs), then release
+            float v[32];
+#pragma unroll
+            for (int c = 0; c < CHUNKS; ++c) {
+                tmem_ld_32x32b_x32(taddr + c * 32, v);
+                tmem_wait_ld();
+                acc[0].x += v[0] * 0.0f;  // keep the loads live
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (PAIR)
+                    mbar_arrive_cluster(&tempty[buf], 0);
+                else
+                    mbar_arrive(&tempty[buf]);
+            }
+            continue;
+        }
         // Software-pipelined: the tcgen05.ld of chunk c+1 is in flight while chunk c's FMAs
         // issue, so each TMEM load latency after the first overlaps useful work.
         float v[2][32];
