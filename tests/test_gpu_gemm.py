@@ -310,3 +310,34 @@ def test_skinny_streamk_path_when_cluster_split_disabled():
     r = subprocess.run([sys.executable, "-c", _STREAMK_SCRIPT], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "streamk ok" in r.stdout, r.stdout + r.stderr
+
+
+_KIND_SCRIPT = r"""
+import numpy as np, torch, oracle
+from tests.test_gpu_gemm import _operands, _run
+from tests.helpers import rel_frobenius
+for i, (m, n, k) in enumerate([(512, 512, 512), (300, 1000, 384), (1024, 2048, 1024)]):
+    a, sa, b, sb = _operands(m, n, k, 90 + i)
+    y = _run(a, sa, b, sb)
+    rows = np.unique(np.r_[0, m - 1, np.random.default_rng(i).integers(0, m, 16)])
+    got = y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert rel_frobenius(got, oracle.gemm_rows(a, sa, b, sb, rows)) <= 1e-5, (m, n, k)
+    yb = _run(a, sa, b, sb, torch.bfloat16)  # the BF16 store path (store warps / staging)
+    assert torch.equal(yb.view(torch.int16), y.to(torch.bfloat16).view(torch.int16))
+print("kind ok")
+"""
+
+
+@pytest.mark.parametrize("kind", ["128", "256", "1128", "2256"])
+def test_gemm_dev_kinds(kind):
+    # The dev tile kinds (FP8Q_GEMM_KIND; production picks 1256 / 256 / the decode kernel) stay
+    # correct and terminate -- kind 1128 once hung (its store warps waited for slices the
+    # 128-column promotion path never parks).  A fresh process per kind: the override is read once.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FP8Q_GEMM_KIND=kind, PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _KIND_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "kind ok" in r.stdout, r.stdout + r.stderr
