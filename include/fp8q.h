@@ -178,14 +178,18 @@ fp8q_status silu_mul_quantize_act_per_token_group(const void* gate_up_bf16, int6
  *   workspace / workspace_bytes: optional (NULL / 0 allowed).  With at least
  *           fp8_block_gemm_workspace_size(m, n, k) bytes (256-byte aligned, ZERO-FILLED before
  *           its first use; every launch leaves it zeroed again), small-M problems (decode,
- *           M <= 128) split the K loop over more CTAs: slices park fp32 partials in the
- *           workspace and the last slice of each tile sums them in slice order
- *           (deterministic).  Without it the same problem runs unsplit (slower, equally
- *           correct).  A workspace must not be shared by concurrently running GEMMs.
+ *           M <= 128) whose weight has many 128-row tiles split the K loop over more CTAs
+ *           (stream-K): slices park fp32 partials in the workspace and the last slice of each
+ *           tile sums them in slice order (deterministic).  Without it the same problem runs
+ *           unsplit (slower, equally correct).  A workspace must not be shared by concurrently
+ *           running GEMMs.  Weights with few tiles (tiles <= SMs / 2) split K inside a thread-
+ *           block cluster instead (partials reduced in CTA-rank order through distributed
+ *           shared memory) and never touch the workspace.
  *   Kernels: 1 <= m <= 128 with 16-byte-aligned a_scales and ld_sa % 4 == 0 runs the swap-AB
- *     decode kernel (weight rows in the MMA M dimension, tokens in N); otherwise the
- *     128 x 256 / 256 x 256 (CTA pair) tile kernel.  Both compute the same per-k-block
- *     promotion in the same k order.
+ *     decode kernel (weight rows in the MMA M dimension, tokens in N), and so does
+ *     129 <= m <= 256 where its cluster split-K applies; otherwise the 128 x 256 / 256 x 256
+ *     (CTA pair) tile kernel.  All compute the same per-k-block promotion in the same k order
+ *     (split-K partial sums are added in a fixed order: results are deterministic).
  *   Requirements: k % 128 == 0, n % 8 == 0 (ESHAPE); a, b 16-byte aligned with ld_a % 16 ==
  *     0 and ld_b % 16 == 0 (TMA); d 16-byte aligned with ld_d * sizeof(out) % 16 == 0;
  *     a_scales/b_scales 4-byte aligned (EALIGN).  m == 0 or n == 0 is a no-op; k == 0 writes 0.
