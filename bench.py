@@ -195,40 +195,52 @@ class LayerStep:
                               out=self.y[name])
 
     def run_e2e(self):
-        """The step through the same C-ABI calls with host (pinned) inputs and outputs: H2D on
-        one copy stream (weights first, then each GEMM's activations), D2H of each GEMM's
-        output on another as soon as it is produced -- PCIe is full duplex, so the output
-        read-back overlaps the remaining input uploads and the compute."""
+        """The step through the same C-ABI calls with host (pinned) inputs and outputs, as a
+        per-GEMM pipeline over four streams: H2D uploads each GEMM's weight shard then its
+        activations (qkv first); the weight sync quantizes (and gathers) each tensor as soon as
+        its shard has landed (buckets of one tensor); each GEMM -- with its activation
+        quantization -- runs on a GEMM stream as soon as its FP8 weight and its activations are
+        there; D2H reads each output back as soon as it is produced.  PCIe is full duplex, so the
+        read-back of the first outputs overlaps the upload of the later weights."""
         fq = self.fp8q
         cur = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_h2d"):
             self._h2d = torch.cuda.Stream(self.device)
             self._d2h = torch.cuda.Stream(self.device)
-        h2d, d2h = self._h2d, self._d2h
+            self._gs = torch.cuda.Stream(self.device)
+        h2d, d2h, gs = self._h2d, self._d2h, self._gs
         h2d.wait_stream(cur)
-        ev_x = {}
+        gs.wait_stream(cur)
+        ev_w, ev_x, ev_q = {}, {}, {}
         with torch.cuda.stream(h2d):
-            for name in self.w:
+            for name, _, _ in LAYER:
                 self.w[name].copy_(self.h_w[name], non_blocking=True)
-            ev_w = torch.cuda.Event()
-            ev_w.record(h2d)
-            for name in self.x:
+                ev_w[name] = torch.cuda.Event()
+                ev_w[name].record(h2d)
                 self.x[name].copy_(self.h_x[name], non_blocking=True)
                 ev_x[name] = torch.cuda.Event()
                 ev_x[name].record(h2d)
-        cur.wait_event(ev_w)
+
+        def quantized(names):
+            for nm in names:
+                ev_q[nm] = torch.cuda.Event()
+                ev_q[nm].record(torch.cuda.current_stream(self.device))
+
         self.step_id += 1
-        self.engine.sync_step(self.step_id, self.w, self.comm)
+        self.engine.sync_step(self.step_id, self.w, self.comm, bucket=1, ready=ev_w, on_bucket=quantized)
         for name, _, _ in LAYER:
-            cur.wait_event(ev_x[name])
-            fq.quantize_act_per_token_group(self.x[name], self.xq[name], self.xs[name])
-            fq.fp8_block_gemm(self.xq[name], self.xs[name], self.engine.codes[name], self.engine.scales[name],
-                              out=self.y[name])
-            ev_y = torch.cuda.Event()
-            ev_y.record(cur)
+            with torch.cuda.stream(gs):
+                gs.wait_event(ev_x[name])
+                gs.wait_event(ev_q[name])
+                fq.quantize_act_per_token_group(self.x[name], self.xq[name], self.xs[name])
+                fq.fp8_block_gemm(self.xq[name], self.xs[name], self.engine.codes[name], self.engine.scales[name],
+                                  out=self.y[name])
+                ev_y = torch.cuda.Event()
+                ev_y.record(gs)
             d2h.wait_event(ev_y)
             with torch.cuda.stream(d2h):
                 self.h_y[name].copy_(self.y[name], non_blocking=True)
+        cur.wait_stream(gs)
         cur.wait_stream(d2h)
         cur.wait_stream(h2d)
 

@@ -235,12 +235,15 @@ class WeightSyncEngine:
         return items
 
     def sync_step(self, step: int, shards: Dict[str, torch.Tensor], comm_stream=None,
-                  bucket: int = 16) -> None:
+                  bucket: int = 16, ready=None, on_bucket=None) -> None:
         """One weight synchronisation: quantize every local shard, all-gather.
 
         Buckets of `bucket` tensors: one batched quantizer launch per bucket, then one grouped
         all-gather of that bucket -- on `comm_stream` when given, so bucket i's gather overlaps
-        bucket i+1's quantization on the compute stream."""
+        bucket i+1's quantization on the compute stream.  `ready` (name -> CUDA event): a
+        bucket's quantization first waits for its tensors' events (e.g. their host uploads), so
+        small buckets pipeline with the uploads; `on_bucket(names)` is called on the stream that
+        finished a bucket (after its gather), e.g. to record an event a consumer waits on."""
         if step <= self.loaded_step:
             raise StaleStepError(f"step {step} is not newer than loaded step {self.loaded_step}")
         missing = [s.name for s in self.specs if s.name not in shards]
@@ -262,6 +265,11 @@ class WeightSyncEngine:
         compute = torch.cuda.current_stream(self.device) if overlap else None
         for b0 in range(0, len(self.specs), bucket):
             chunk = self.specs[b0:b0 + bucket]
+            if ready is not None:
+                cs = torch.cuda.current_stream(self.device)
+                for sp in chunk:
+                    if sp.name in ready:
+                        cs.wait_event(ready[sp.name])
             if batched:
                 quantize_weight_blockwise_batched(self._local_items(chunk, shards))
             else:
@@ -274,8 +282,12 @@ class WeightSyncEngine:
                 with torch.cuda.stream(comm_stream):
                     comm_stream.wait_event(ev)
                     self.gather_many(names)
+                    if on_bucket is not None:
+                        on_bucket(names)
             else:
                 self.gather_many(names)
+                if on_bucket is not None:
+                    on_bucket(names)
         if overlap:
             compute.wait_stream(comm_stream)
         self.loaded_step = step
