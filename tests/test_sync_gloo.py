@@ -63,6 +63,20 @@ def _worker(rank, world, port, q):
         except StaleStepError:
             pass
         assert eng.loaded_step == 2
+        # buckets of one tensor with a completion hook (the e2e pipeline's mode): the hook sees
+        # every tensor once, in spec order, after its gather; the bytes are unchanged
+        seen = []
+        shards = {}
+        for s in SPECS:
+            r0, r1 = eng.shard_rows(s.name)
+            shards[s.name] = full_weight(s, 3)[r0:r1].contiguous()
+        eng.sync_step(3, shards, bucket=1, on_bucket=seen.extend)
+        assert seen == [s.name for s in SPECS], seen
+        for s in SPECS:
+            w = full_weight(s, 3).view(torch.int16).numpy().view(np.uint16)
+            oc, os_ = oracle.quantize_weight_blockwise(w, nthreads=2)
+            assert np.array_equal(eng.codes[s.name].numpy(), oc), (rank, s.name, "bucket=1")
+            assert np.array_equal(eng.scales[s.name].numpy(), os_), (rank, s.name, "bucket=1")
         dist.destroy_process_group()
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover
