@@ -512,7 +512,12 @@ __device__ __forceinline__ void aq_load_smem(uint32_t base, int64_t groups, int6
         }
     }
 }
+// kTma: each item is ONE 3-D TMA box (128 BF16 x 16 groups x 1 row of the tensor map
+// {128, groups, m}, groups past the row zero-filled) instead of a cp.async.bulk copy; same
+// shared-memory layout, same consumers.
+template <bool kTma>
 __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kernel(
+    const __grid_constant__ CUtensorMap tmx,
     const uint16_t* __restrict__ x, int64_t ld_x, uint8_t* __restrict__ q, int64_t ld_q,
     float* __restrict__ scales, int64_t ld_s, int64_t groups, int64_t chunks, int64_t items,
     int32_t* __restrict__ nonfinite_flag) {
@@ -551,10 +556,16 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
                 for (int j = 0; j < cnt; ++j) {
                     // copies may complete before the expect_tx below: the phase cannot, since
                     // its one arrival (the expect_tx arrive) is still pending
-                    const uint32_t nb = chunk == nch - 1 ? tail_bytes : 4096u;
-                    bulk_g2s(ring + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, x + row * ld_x + chunk * 2048, nb,
-                             &full[s]);
-                    bytes += nb;
+                    if (kTma) {
+                        tma_load_3d(abq_smem + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, &tmx, &full[s], 0, chunk * 16,
+                                    static_cast<int32_t>(row));
+                        bytes += 4096u;  // the whole box counts, zero-filled groups included
+                    } else {
+                        const uint32_t nb = chunk == nch - 1 ? tail_bytes : 4096u;
+                        bulk_g2s(ring + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, x + row * ld_x + chunk * 2048, nb,
+                                 &full[s]);
+                        bytes += nb;
+                    }
                     if (++chunk == nch) {
                         chunk = 0;
                         ++row;
@@ -881,19 +892,43 @@ cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, 
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev >= 0 && dev < 64 && !attr_done[dev]) {
-            const cudaError_t ea = cudaFuncSetAttribute(act_per_token_group_bulk_kernel,
-                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                        static_cast<int>(ABQ_SMEM));
+            cudaError_t ea = cudaFuncSetAttribute(act_per_token_group_bulk_kernel<false>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(ABQ_SMEM));
+            if (ea == cudaSuccess)
+                ea = cudaFuncSetAttribute(act_per_token_group_bulk_kernel<true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ABQ_SMEM));
             if (ea != cudaSuccess) return ea;
             attr_done[dev] = true;
+        }
+        // dev A/B: FP8Q_ACT_LOAD=bulk keeps the cp.async.bulk copies
+        static const bool act_tma_env = [] {
+            const char* e = std::getenv("FP8Q_ACT_LOAD");
+            return !(e != nullptr && e[0] == 'b');
+        }();
+        const auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encode_fn());
+        CUtensorMap tmx{};
+        bool use_tma = act_tma_env && encode != nullptr;
+        if (use_tma) {
+            cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(groups), static_cast<cuuint64_t>(m)};
+            cuuint64_t strides[2] = {256, static_cast<cuuint64_t>(ld_x) * 2};
+            cuuint32_t box[3] = {128, 16, 1};
+            cuuint32_t estr[3] = {1, 1, 1};
+            use_tma = encode(&tmx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(x), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
         }
         const int64_t wchunks = (groups + 15) / 16;
         const int64_t witems = m * wchunks;
         const int64_t per_cta_min = 2 * ABQ_ITEMS;  // small inputs: fewer CTAs, each a few stages
         int64_t grid = (witems + per_cta_min - 1) / per_cta_min;
         grid = grid < sm_count() ? grid : sm_count();
-        act_per_token_group_bulk_kernel<<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
-            x, ld_x, q, ld_q, scales, ld_s, groups, wchunks, witems, flag);
+        if (use_tma)
+            act_per_token_group_bulk_kernel<true><<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
+                tmx, x, ld_x, q, ld_q, scales, ld_s, groups, wchunks, witems, flag);
+        else
+            act_per_token_group_bulk_kernel<false><<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
+                tmx, x, ld_x, q, ld_q, scales, ld_s, groups, wchunks, witems, flag);
     } else if (al(x, 32) && ld_x % 16 == 0 && al(q, 16) && ld_q % 16 == 0) {
         const int64_t wchunks = (groups + 15) / 16;
         const int64_t witems = m * wchunks;
