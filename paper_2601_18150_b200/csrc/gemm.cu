@@ -100,7 +100,8 @@ struct KParams {
                              // 2 = also no TMA after the first stages (tensor-core-only ceiling),
                              // 3 = (pair) the MMA issuer ignores TMEM buffer releases and the
                              //     promotion/store warps idle: TMA + MMA without the release chain,
-                             // 4 = promotion reads TMEM (all chunks) but does no FMAs
+                             // 4 = promotion reads TMEM (all chunks) but does no FMAs,
+                             // 5 = mode 1 without the tile epilogue (no BF16 parking / stores)
     int groups;
 };
 
@@ -341,6 +342,7 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
     }
     const bool tr_store = (threadIdx.x == EPI_WARP0 * 32);
     if (tr_store) trace_ev(p, it - 1, 6);
+    if (p.debug_mode == 5) return;  // dev: mode 1 without the tile epilogue
     if (!PAIR && p.splits > 1) {
         // ---- split-K: park this slice's fp32 partial; the last slice to arrive sums all
         // slices in slice order (deterministic) and stores the tile.
@@ -877,7 +879,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 mbar_wait(&tempty[i % NBUF], (i / NBUF) & 1u);
             }
         }
-    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128 && p.debug_mode != 3) {
+    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128 && p.debug_mode != 3 &&
+               p.debug_mode != 5) {
         // ------------------------------------------------------------ store warps (BF16)
         // (only where promote_tile parks BF16 slices for them: 128 columns per half; with
         // PBN = 128 the promotion warps store their tile themselves -- gating on out_f32 alone
