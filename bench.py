@@ -23,8 +23,9 @@ the timed region.  `e2e` repeats the step through the same C-ABI calls with HOST
 outputs are inside its timed region.
 
 --impl reference times the CPU oracle (the reference arm of this tier; it is deliberately
-slow) on a bounded sample of the same workload.  Other workloads (--workload sync30b,
-decode, moe) print their own lines for the other configs.
+slow) on a bounded sample of the same workload.  --workload sync8b|sync30b prints the
+whole-model weight-sync line (BASELINE.json configs[4]); the decode (configs[2]) and MoE
+(configs[3]) GEMMs are measured by tools/kernel_bench.py --decode --graph / --moe.
 """
 from __future__ import annotations
 
