@@ -301,6 +301,17 @@ fp8q_status fp8_mx_gemm(const uint8_t* a, int64_t ld_a, const uint8_t* a_scales,
                         int64_t k, void* stream);
 
 /*
+ * e4m3_encode_f32 -- the element encode of every quantizer above (step a3, Eq. (1)
+ *   "round", readings Q1/Q7/Q9): codes[i] = E4M3_RNE_satfinite(x[i]) through the same
+ *   hardware `cvt.rn.satfinite.e4m3x2.f32` instruction and the same device helper the
+ *   quantizers use, applied to raw fp32 values (no scale).  Exposed so the encode can be
+ *   checked against the oracle on all 2^32 fp32 bit patterns (SURVEY §8(c) O2 pin (iv)).
+ *   x [n] fp32, codes [n] bytes out (device).  n >= 0; n > 0 requires x 8-byte and codes
+ *   2-byte aligned and n % 2 == 0 (EALIGN / ESHAPE).  NaN input gives a NaN code.
+ */
+fp8q_status e4m3_encode_f32(const float* x, int64_t n, uint8_t* codes, void* stream);
+
+/*
  * fp8q_kernel_launches -- number of kernels this library has launched in this process
  * (monotone counter; used by bench.py to report `gpu_launches`).
  */

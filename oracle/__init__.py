@@ -48,6 +48,8 @@ def _load():
             lib.oracle_e4m3_decode.restype = ctypes.c_double
             lib.oracle_e4m3_encode.argtypes = [ctypes.c_float]
             lib.oracle_e4m3_encode.restype = ctypes.c_uint8
+            lib.oracle_e4m3_encode_array.argtypes = [P, I64, P, ctypes.c_int]
+            lib.oracle_e4m3_encode_array.restype = None
             lib.oracle_block_scale.argtypes = [ctypes.c_float]
             lib.oracle_block_scale.restype = ctypes.c_float
             lib.oracle_quantize_element.argtypes = [ctypes.c_float, ctypes.c_float]
@@ -105,6 +107,14 @@ def e4m3_decode_table() -> np.ndarray:
 def e4m3_encode(q: float) -> int:
     """O2: nearest E4M3, ties-to-even code, saturating, sign kept."""
     return _load().oracle_e4m3_encode(float(np.float32(q)))
+
+
+def e4m3_encode_array(q: np.ndarray, nthreads: int | None = None) -> np.ndarray:
+    """O2 applied to every element of a float32 array (the same scalar function)."""
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    out = np.empty(q.shape, dtype=np.uint8)
+    _load().oracle_e4m3_encode_array(_ptr(q), q.size, _ptr(out), nthreads or default_threads())
+    return out
 
 
 def block_scale(amax: float) -> np.float32:

@@ -101,6 +101,13 @@ uint8_t oracle_e4m3_encode(float q) {
     return sign | (uint8_t)code;
 }
 
+/* O2 over an array (for the all-2^32 hardware comparison; same function per element). */
+typedef struct {
+    const float* q;
+    uint8_t* out;
+} enc_ctx;
+static void enc_range(void* p, int64_t begin, int64_t end);
+
 /* BF16 is the upper half of a binary32: widening is exact. */
 float oracle_bf16_to_float(uint16_t h) {
     uint32_t u = ((uint32_t)h) << 16;
@@ -164,6 +171,16 @@ static void parallel_for(range_fn fn, void* ctx, int64_t total, int nthreads) {
     }
     for (int t = 0; t < launched; ++t)
         if (jobs[t].fn) pthread_join(th[t], NULL);
+}
+
+static void enc_range(void* p, int64_t begin, int64_t end) {
+    enc_ctx* c = (enc_ctx*)p;
+    for (int64_t i = begin; i < end; ++i) c->out[i] = oracle_e4m3_encode(c->q[i]);
+}
+
+void oracle_e4m3_encode_array(const float* q, int64_t n, uint8_t* out, int nthreads) {
+    enc_ctx c = {q, out};
+    parallel_for(enc_range, &c, n, nthreads);
 }
 
 /* ------------------------------------------------------------------ weights (O3-O6) */
@@ -280,13 +297,20 @@ typedef struct {
     double* out;
 } gemm_ctx;
 
+/* Work items are (row, 64-column block) pairs so that a small row sample still spreads over
+ * every host thread; each output element is computed exactly as written above (same
+ * operands, same k order) whichever thread owns it. */
+#define GEMM_COLS_PER_ITEM 64
 static void gemm_range(void* p, int64_t begin, int64_t end) {
     gemm_ctx* c = (gemm_ctx*)p;
     pthread_once(&g_tab_once, build_table);
-    for (int64_t r = begin; r < end; ++r) {
+    int64_t ncb = (c->n + GEMM_COLS_PER_ITEM - 1) / GEMM_COLS_PER_ITEM;
+    for (int64_t item = begin; item < end; ++item) {
+        int64_t r = item / ncb, cb = item % ncb;
         int64_t row = c->rows[r];
         const uint8_t* ar = c->a + row * c->ld_a;
-        for (int64_t col = 0; col < c->n; ++col) {
+        int64_t col1 = (cb + 1) * GEMM_COLS_PER_ITEM < c->n ? (cb + 1) * GEMM_COLS_PER_ITEM : c->n;
+        for (int64_t col = cb * GEMM_COLS_PER_ITEM; col < col1; ++col) {
             const uint8_t* br = c->b + col * c->ld_b;
             double acc = 0.0;
             for (int64_t kk = 0; kk < c->k; ++kk) {
@@ -305,7 +329,7 @@ int oracle_gemm_rows(const uint8_t* a, int64_t ld_a, const float* sa, int64_t ld
                      int64_t k, const int64_t* rows, int64_t nrows, double* out, int nthreads) {
     if (n < 0 || k < 0 || k % 128 != 0 || nrows < 0) return ORACLE_EINVAL;
     gemm_ctx c = {a, ld_a, sa, ld_sa, b, ld_b, sb, ld_sb, n, k, rows, out};
-    parallel_for(gemm_range, &c, nrows, nthreads);
+    parallel_for(gemm_range, &c, nrows * ((n + GEMM_COLS_PER_ITEM - 1) / GEMM_COLS_PER_ITEM), nthreads);
     return ORACLE_OK;
 }
 

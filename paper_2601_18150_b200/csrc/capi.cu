@@ -53,6 +53,19 @@ int32_t fp8q_version(void) { return 10000; }
 
 int64_t fp8q_kernel_launches(void) { return g_launches.load(); }
 
+fp8q_status e4m3_encode_f32(const float* x, int64_t n, uint8_t* codes, void* stream) {
+    if (n < 0) return FP8Q_EINVAL;
+    if (n == 0) return FP8Q_OK;
+    if (x == nullptr || codes == nullptr) return FP8Q_EINVAL;
+    if (n % 2 != 0) return FP8Q_ESHAPE;
+    if (!aligned(x, 8) || !aligned(codes, 2)) return FP8Q_EALIGN;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    cudaError_t e = fp8q::launch_e4m3_encode(x, n, codes, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return from_cuda(e);
+}
+
 void fp8q_debug_set_gemm_trace(uint32_t* dev_ptr) { fp8q::set_gemm_trace(dev_ptr); }
 
 static fp8q_status check_weight(const void* w_bf16, int64_t n, int64_t k, int64_t ld_w, const uint8_t* codes,

@@ -866,6 +866,27 @@ int weight_batch_launches(const WeightDesc* descs, int count) {
     return narrow + (wide + kMaxWeightBatch - 1) / kMaxWeightBatch;
 }
 
+namespace {
+// a3 on raw fp32 pairs: the quantizers' cvt_e4m3x2 helper (element i -> byte i), grid-stride.
+__global__ void __launch_bounds__(256) e4m3_encode_kernel(const float2* __restrict__ x, int64_t pairs,
+                                                          uint16_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < pairs;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const float2 v = x[i];
+        out[i] = static_cast<uint16_t>(cvt_e4m3x2(v.x, v.y));
+    }
+}
+}  // namespace
+
+cudaError_t launch_e4m3_encode(const float* x, int64_t n, uint8_t* codes, cudaStream_t stream) {
+    const int64_t pairs = n / 2;
+    int64_t blocks = (pairs + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    e4m3_encode_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        reinterpret_cast<const float2*>(x), pairs, reinterpret_cast<uint16_t*>(codes));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int64_t ld_w,
                                     uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
                                     int32_t* flag, cudaStream_t stream) {

@@ -28,6 +28,9 @@ cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int
                                     uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
                                     int32_t* flag, cudaStream_t stream);
 
+// a3 element encode on raw fp32 pairs (e4m3_encode_f32): the quantizers' cvt helper.
+cudaError_t launch_e4m3_encode(const float* x, int64_t n, uint8_t* codes, cudaStream_t stream);
+
 cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, int64_t ld_x,
                                        uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
                                        int32_t* flag, cudaStream_t stream);

@@ -58,6 +58,8 @@ def load_library() -> ctypes.CDLL:
         lib.quantize_weight_blockwise_batched.restype = ctypes.c_int
         lib.quantize_weight_blockwise_fanout.argtypes = [ctypes.POINTER(WeightTensorDesc), I32, I32, P, P, P, P]
         lib.quantize_weight_blockwise_fanout.restype = ctypes.c_int
+        lib.e4m3_encode_f32.argtypes = [P, I64, P, P]
+        lib.e4m3_encode_f32.restype = ctypes.c_int
         lib.quantize_act_per_token_group.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
         lib.quantize_act_per_token_group.restype = ctypes.c_int
         lib.rmsnorm_quantize_act_per_token_group.argtypes = [P, P, ctypes.c_float, I64, I64, I64, P, I64, P, I64,
@@ -197,6 +199,20 @@ def quantize_weight_blockwise_fanout(items, codes_delta, scales_delta, nonfinite
            "quantize_weight_blockwise_fanout")
 
 
+def e4m3_encode_f32(x: torch.Tensor, codes: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Step a3 alone: E4M3_RNE_satfinite of raw fp32 values through the
+    quantizers' hardware cvt -- for checking the encode on every fp32 bit pattern."""
+    if not (x.is_cuda and x.dtype == torch.float32 and x.dim() == 1 and x.is_contiguous()):
+        raise Fp8qError("x must be a contiguous 1-D CUDA float32 tensor")
+    if codes is None:
+        codes = torch.empty(x.numel(), dtype=torch.uint8, device=x.device)
+    if not (codes.is_cuda and codes.dtype == torch.uint8 and codes.is_contiguous() and codes.numel() == x.numel()):
+        raise Fp8qError("codes must be a contiguous CUDA uint8 tensor with x.numel() elements")
+    _check(load_library().e4m3_encode_f32(x.data_ptr(), x.numel(), codes.data_ptr(), _stream(stream)),
+           "e4m3_encode_f32")
+    return codes
+
+
 def act_scales_ld(m: int) -> int:
     """Leading dimension of the MN-major activation-scale array (>= m, multiple of 4)."""
     return max(4, (m + 3) // 4 * 4)
@@ -246,6 +262,8 @@ def rmsnorm_quantize_act_per_token_group(x: torch.Tensor, gamma: torch.Tensor, e
     if not (gamma.is_cuda and gamma.dtype == torch.bfloat16 and gamma.dim() == 1 and gamma.is_contiguous()):
         raise Fp8qError("gamma must be a contiguous CUDA bfloat16 vector")
     m, k = x.shape
+    if gamma.numel() != k:
+        raise Fp8qError(f"gamma must have k={k} elements, got {gamma.numel()}")
     codes, scales = _act_outputs(m, k, x.device, codes, scales)
     y_ptr, ld_y = (None, 0)
     if y_out is not None:
@@ -294,16 +312,47 @@ def _out(out, m, n, out_dtype, device):
 _WS: dict = {}
 
 
-def _workspace(device, stream_handle: int, nbytes: int):
-    """Zero-filled split-K workspace cached per (device, stream); the kernels leave it zeroed."""
+def _stream_obj(stream, device) -> torch.cuda.Stream:
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if isinstance(stream, torch.cuda.Stream):
+        return stream
+    return torch.cuda.ExternalStream(int(stream), device=device)
+
+
+def _workspace(device, stream, nbytes: int):
+    """Zero-filled split-K workspace cached per (device, stream); the kernels leave it zeroed.
+
+    Allocated and zero-filled ON the stream the GEMM runs on, so the caching allocator ties the
+    block to that stream: the memset is ordered before the GEMM, and a replaced (smaller)
+    workspace is only recycled for later work on the same stream, after the GEMMs that used it."""
     if nbytes == 0:
         return None, 0
-    key = (device.index, stream_handle)
+    st = _stream_obj(stream, device)
+    key = (device.index, st.cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        with torch.cuda.stream(st):
+            ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws.data_ptr(), ws.numel()
+
+
+def _check_act_scales(sc: torch.Tensor, m: int, k: int, name: str) -> int:
+    """MN-major activation scales [k/128, ld_s >= m]: returns ld_s."""
+    _cuda2d(sc, name, torch.float32)
+    if sc.shape[0] < k // 128 or (sc.shape[1] < m and m > 0):
+        raise Fp8qError(f"{name} must be at least [k/128={k // 128}, m={m}], got {tuple(sc.shape)}")
+    return sc.stride(0) if sc.shape[0] > 1 else sc.shape[1]
+
+
+def _check_weight_scales(sc: torch.Tensor, n: int, k: int, name: str) -> int:
+    """Weight scales [ceil(n/128), >= k/128]: returns ld_sb."""
+    _cuda2d(sc, name, torch.float32)
+    if sc.shape[0] < (n + 127) // 128 or sc.shape[1] < k // 128:
+        raise Fp8qError(f"{name} must be at least [ceil(n/128)={(n + 127) // 128}, k/128={k // 128}], "
+                        f"got {tuple(sc.shape)}")
+    return sc.stride(0) if sc.shape[0] > 1 else sc.shape[1]
 
 
 def fp8_block_gemm(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_scales: torch.Tensor,
@@ -320,11 +369,11 @@ def fp8_block_gemm(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_s
     if kb != k:
         raise Fp8qError("fp8_block_gemm: inner dimensions differ")
     out = _out(out, m, n, out_dtype, a.device)
-    ld_sa = a_scales.stride(0) if a_scales.shape[0] > 1 else a_scales.shape[1]
-    ld_sb = b_scales.stride(0) if b_scales.shape[0] > 1 else b_scales.shape[1]
+    ld_sa = _check_act_scales(a_scales, m, k, "a_scales")
+    ld_sb = _check_weight_scales(b_scales, n, k, "b_scales")
     lib = load_library()
     sh = _stream(stream)
-    ws_ptr, ws_bytes = _workspace(a.device, sh, int(lib.fp8_block_gemm_workspace_size(m, n, k)))
+    ws_ptr, ws_bytes = _workspace(a.device, stream, int(lib.fp8_block_gemm_workspace_size(m, n, k)))
     _check(lib.fp8_block_gemm(
         a.data_ptr(), _ld(a), a_scales.data_ptr(), ld_sa, b.data_ptr(), _ld(b), b_scales.data_ptr(),
         ld_sb, out.data_ptr(), _ld(out), FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16,
@@ -353,7 +402,10 @@ def fp8_block_gemm_grouped(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Ten
     if a.shape[1] != k:
         raise Fp8qError("inner dimensions differ")
     out = _out(out, m, n, out_dtype, a.device)
-    ld_sa = a_scales.stride(0) if a_scales.shape[0] > 1 else a_scales.shape[1]
+    ld_sa = _check_act_scales(a_scales, m, k, "a_scales")
+    if b_scales.shape[0] < G or b_scales.shape[1] < (n + 127) // 128 or b_scales.shape[2] < k // 128:
+        raise Fp8qError(f"b_scales must be at least [G={G}, ceil(n/128)={(n + 127) // 128}, k/128={k // 128}], "
+                        f"got {tuple(b_scales.shape)}")
     _check(load_library().fp8_block_gemm_grouped(
         a.data_ptr(), _ld(a), a_scales.data_ptr(), ld_sa, b.data_ptr(), b.stride(1), b.stride(0),
         b_scales.data_ptr(), b_scales.stride(1), b_scales.stride(0), out.data_ptr(), _ld(out),
@@ -422,8 +474,14 @@ def mx_quantize(x: torch.Tensor, codes: torch.Tensor | None = None, scales: torc
     lib = load_library()
     if codes is None:
         codes = torch.empty((rows, k), dtype=torch.uint8, device=x.device)
+    need = int(lib.mx_scale_bytes(rows, k))
     if scales is None:
-        scales = torch.empty(max(1, int(lib.mx_scale_bytes(rows, k))), dtype=torch.uint8, device=x.device)
+        scales = torch.empty(max(1, need), dtype=torch.uint8, device=x.device)
+    _cuda2d(codes, "codes", torch.uint8)
+    if codes.shape != (rows, k):
+        raise Fp8qError("codes shape mismatch")
+    if not (scales.is_cuda and scales.dtype == torch.uint8 and scales.is_contiguous() and scales.numel() >= need):
+        raise Fp8qError(f"scales must be a contiguous CUDA uint8 buffer of >= mx_scale_bytes = {need} bytes")
     _check(lib.mx_quantize(x.data_ptr(), rows, k, _ld(x), codes.data_ptr(), _ld(codes), scales.data_ptr(),
                            _opt_ptr(nonfinite_flag, "nonfinite_flag", torch.int32), _stream(stream)), "mx_quantize")
     return codes, scales
@@ -439,6 +497,11 @@ def fp8_mx_gemm(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_scal
     if b.shape[1] != k:
         raise Fp8qError("fp8_mx_gemm: inner dimensions differ")
     out = _out(out, m, n, out_dtype, a.device)
+    lib = load_library()
+    for t, rows, nm in ((a_scales, m, "a_scales"), (b_scales, n, "b_scales")):
+        need = int(lib.mx_scale_bytes(rows, k))
+        if not (t.is_cuda and t.dtype == torch.uint8 and t.is_contiguous() and t.numel() >= need):
+            raise Fp8qError(f"{nm} must be a contiguous CUDA uint8 buffer of >= mx_scale_bytes = {need} bytes")
     _check(load_library().fp8_mx_gemm(a.data_ptr(), _ld(a), a_scales.data_ptr(), b.data_ptr(), _ld(b),
                                       b_scales.data_ptr(), out.data_ptr(), _ld(out),
                                       FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16, m, n, k,

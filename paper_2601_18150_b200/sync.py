@@ -30,6 +30,11 @@ class StaleStepError(RuntimeError):
     """sync_step called with a step not newer than the loaded one."""
 
 
+class NonFiniteWeightError(RuntimeError):
+    """A shard held NaN/Inf (non-finite input is rejected).  The engine buffers are
+    then undefined (`engine.poisoned`) and `loaded_step` is not advanced."""
+
+
 @dataclasses.dataclass(frozen=True)
 class TensorSpec:
     """One quantized linear weight.  Dense: [n, k] (nn.Linear [out, in]).  MoE experts:
@@ -151,9 +156,9 @@ def symmetric_peer_buffers(specs, device, group=None) -> PeerBuffers:
     return PeerBuffers(c, s, cd, sd, fence=lambda: hc.barrier(), keep=(c, s, hc, hs))
 
 
-def _default_quantize(w: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor) -> None:
+def _default_quantize(w: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor, flag=None) -> None:
     from .fp8q import quantize_weight_blockwise
-    quantize_weight_blockwise(w, codes, scales)
+    quantize_weight_blockwise(w, codes, scales, nonfinite_flag=flag)
 
 
 class WeightSyncEngine:
@@ -185,6 +190,11 @@ class WeightSyncEngine:
                 self.scales[s.name] = torch.empty((s.scale_rows, s.scale_cols), dtype=torch.float32,
                                                   device=self.device)
         self.loaded_step = -1
+        # device int32, set by every quantizer launch that meets a NaN/Inf (fp8q.h contract);
+        # read before loaded_step advances (strict) or by check_finite() (deferred)
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device) \
+            if self.device.type == "cuda" else None
+        self.poisoned = False
 
     def my_shard(self, name: str) -> Shard:
         return self.plans[name][self.rank]
@@ -224,18 +234,49 @@ class WeightSyncEngine:
             for n in names:
                 self.gather(n)
 
+    def _validate(self, shards: Dict[str, torch.Tensor]) -> None:
+        """Every shard's presence, shape, dtype and device, checked before anything is launched
+        or any collective is entered, so a bad shard never leaves a half-synced engine (or a
+        rank that skips collectives its peers are blocked in)."""
+        missing = [s.name for s in self.specs if s.name not in shards]
+        if missing:
+            raise KeyError(f"missing shards: {missing}")
+        for s in self.specs:
+            sh = self.my_shard(s.name)
+            w = shards[s.name]
+            want = (sh.row1 - sh.row0, s.k)
+            if tuple(w.shape) != want:
+                raise ValueError(f"{s.name}: shard shape {tuple(w.shape)}, plan says {want}")
+            if w.dtype != torch.bfloat16:
+                raise ValueError(f"{s.name}: shard dtype {w.dtype}, expected torch.bfloat16")
+            if w.device != self.codes[s.name].device:
+                raise ValueError(f"{s.name}: shard on {w.device}, engine buffers on {self.codes[s.name].device}")
+
     def _local_items(self, specs, shards):
         items = []
         for s in specs:
             sh = self.my_shard(s.name)
-            w = shards[s.name]
-            if w.shape[0] != sh.row1 - sh.row0:
-                raise ValueError(f"{s.name}: shard has {w.shape[0]} rows, plan says {sh.row1 - sh.row0}")
-            items.append((w, self.codes[s.name][sh.row0:sh.row1], self.scales[s.name][sh.srow0:sh.srow1]))
+            items.append((shards[s.name], self.codes[s.name][sh.row0:sh.row1],
+                          self.scales[s.name][sh.srow0:sh.srow1]))
         return items
 
+    def check_finite(self) -> None:
+        """Deferred non-finite check (for sync_step(strict=False)): raises NonFiniteWeightError
+        if any quantizer launch since the last check met a NaN/Inf, on every rank alike (the
+        flag is MAX-reduced over the group), and re-arms the flag.  Host-synchronising."""
+        if self.nonfinite is None:
+            return
+        f = self.nonfinite.clone()
+        if self.world > 1:
+            dist.all_reduce(f, op=dist.ReduceOp.MAX, group=self.group)
+        bad = int(f.item()) != 0
+        self.nonfinite.zero_()
+        if bad:
+            self.poisoned = True
+            raise NonFiniteWeightError("non-finite BF16 weight in a synced shard; engine buffers undefined")
+
     def sync_step(self, step: int, shards: Dict[str, torch.Tensor], comm_stream=None,
-                  bucket: int = 16, ready=None, on_bucket=None) -> None:
+                  bucket: int = 16, ready=None, on_bucket=None, strict: bool = True) -> None:
         """One weight synchronisation: quantize every local shard, all-gather.
 
         Buckets of `bucket` tensors: one batched quantizer launch per bucket, then one grouped
@@ -243,20 +284,30 @@ class WeightSyncEngine:
         bucket i+1's quantization on the compute stream.  `ready` (name -> CUDA event): a
         bucket's quantization first waits for its tensors' events (e.g. their host uploads), so
         small buckets pipeline with the uploads; `on_bucket(names)` is called on the stream that
-        finished a bucket (after its gather), e.g. to record an event a consumer waits on."""
+        finished a bucket (after its gather), e.g. to record an event a consumer waits on.
+
+        Non-finite input sets the engine's device flag in the quantizer.  strict:
+        the flag is read (MAX over ranks) before `loaded_step` advances -- a host sync -- and a
+        NonFiniteWeightError leaves `loaded_step` unchanged.  strict=False: no host sync; call
+        check_finite() later (the flag accumulates until then)."""
         if step <= self.loaded_step:
             raise StaleStepError(f"step {step} is not newer than loaded step {self.loaded_step}")
-        missing = [s.name for s in self.specs if s.name not in shards]
-        if missing:
-            raise KeyError(f"missing shards: {missing}")
+        self._validate(shards)
+        flag = self.nonfinite
+        if strict and flag is not None:
+            flag.zero_()
         if self.peers is not None:
-            # NEXT-1: the quantizer writes every rank's buffer itself; no gather pass
+            # NEXT-1: the quantizer writes every rank's buffer itself; no gather pass.  The
+            # opening fence keeps a fast rank from overwriting a peer's step-t weights while the
+            # peer may still be reading them; the closing fence publishes every rank's stores.
             from .fp8q import quantize_weight_blockwise_fanout
+            self.peers.fence()
             for b0 in range(0, len(self.specs), bucket):
                 quantize_weight_blockwise_fanout(self._local_items(self.specs[b0:b0 + bucket], shards),
-                                                 self.peers.codes_delta, self.peers.scales_delta)
+                                                 self.peers.codes_delta, self.peers.scales_delta,
+                                                 nonfinite_flag=flag)
             self.peers.fence()
-            self.loaded_step = step
+            self._commit(step, strict)
             return
         batched = self.quantize_fn is _default_quantize
         if batched:
@@ -271,7 +322,7 @@ class WeightSyncEngine:
                     if sp.name in ready:
                         cs.wait_event(ready[sp.name])
             if batched:
-                quantize_weight_blockwise_batched(self._local_items(chunk, shards))
+                quantize_weight_blockwise_batched(self._local_items(chunk, shards), nonfinite_flag=flag)
             else:
                 for s in chunk:
                     self.quantize_local(s.name, shards[s.name])
@@ -290,4 +341,10 @@ class WeightSyncEngine:
                     on_bucket(names)
         if overlap:
             compute.wait_stream(comm_stream)
+        self._commit(step, strict)
+
+    def _commit(self, step: int, strict: bool) -> None:
+        if strict:
+            self.check_finite()
+        self.poisoned = False
         self.loaded_step = step
