@@ -178,14 +178,17 @@ def max_over_ranks(x: float, device, world) -> float:
 
 
 class L2Flush:
-    """A 256 MB write between timed launches: every timed kernel starts with L2 holding other
-    (dirty) data, as it would after the producer of its inputs."""
+    """Between timed launches: write a 256 MB buffer (> 126 MB L2), then read it back, so every
+    timed kernel starts with a cold L2 that holds other, CLEAN data.  (A write alone leaves
+    ~126 MB of dirty lines whose write-back the next kernel pays: ~20 us, which dominated the
+    small shard / expert GEMMs in the first round-2 bench line.)"""
 
     def __init__(self, device):
         self.buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
 
     def __call__(self):
         self.buf.zero_()
+        self.buf.view(torch.int64).sum()
 
 
 def time_launch(fn, flush: L2Flush, iters: int = 10, warm: int = 2) -> float:
@@ -278,8 +281,8 @@ class LayerStep:
         self.engine.sync_step(self.step_id, self.w, self.comm, strict=False)
         if ev:
             ev[1].record()
-        for name, _, _ in LAYER:
-            fq.quantize_act_per_token_group(self.x[name], self.xq[name], self.xs[name])
+        # the layer's four GEMM inputs in one persistent launch
+        fq.quantize_act_per_token_group_batched([(self.x[nm], self.xq[nm], self.xs[nm]) for nm, _, _ in LAYER])
         if ev:
             ev[2].record()
         for name, _, _ in LAYER:
@@ -475,7 +478,7 @@ def bench_moe(device, peaks, clocks, flush, tokens=(1024, 8192), iters=10):
     del experts
     return {"config": "BASELINE.json configs[3]: Qwen3-30B-A3B experts (128 x fc1 [1536,2048], fc2 [2048,768]), "
                       "top-8 routing, bf16 out",
-            "timing": f"CUDA events per launch after a 256 MB L2 flush, median of {iters}",
+            "timing": f"CUDA events per launch after a 256 MB L2 flush (write + read back: cold, clean L2), median of {iters}",
             "roofline": {"bound": "max(tensor, hbm) per case", "tensor_peak_tflops": round(peak, 1),
                          "hbm_peak_gbs": peaks["hbm_gbs"],
                          "note": "tensor peak = 2 x measured bf16 BURST (kernels timed alone)"},
@@ -614,7 +617,7 @@ def bench_tp_shards(st: LayerStep, peaks, clocks, flush, ps=(2, 4, 8), iters=10)
             res[f"{model}_P{P}"] = rec
     del weights, w30, x2048
     return {"config": "column-parallel shard GEMMs (N/P rows of each weight, replicated M = 8192 activations)",
-            "timing": f"CUDA events per launch after a 256 MB L2 flush, median of {iters}",
+            "timing": f"CUDA events per launch after a 256 MB L2 flush (write + read back: cold, clean L2), median of {iters}",
             "roofline": {"bound": "tensor", "peak": round(peak, 1), "unit": "TFLOP/s",
                          "peak_source": "2 x measured bf16 BURST (kernels timed alone)"},
             "results": res, "clocks": clocks.summary(t_win, time.perf_counter())}

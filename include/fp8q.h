@@ -140,6 +140,30 @@ fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t 
                                          int32_t* nonfinite_flag, void* stream);
 
 /*
+ * quantize_act_per_token_group_batched -- the activation quantizations of one forward step
+ * (every linear layer's input is quantized dynamically) issued together: does
+ * exactly what `count` quantize_act_per_token_group calls would do, but in as few kernel
+ * launches as possible (up to 8 tensors per persistent launch), so the inputs of a layer's
+ * GEMMs share one pipeline ramp and one tail.
+ *   tensors  HOST array of `count` descriptors (read during the call only); the pointers in
+ *            them are device pointers with the meaning and requirements of
+ *            quantize_act_per_token_group.  Every descriptor is validated before anything is
+ *            enqueued; the first failing one determines the status.
+ *   nonfinite_flag, stream  as quantize_act_per_token_group (one flag for the whole batch).
+ */
+typedef struct {
+    const void* x_bf16;
+    int64_t m, k, ld_x;
+    uint8_t* codes;
+    int64_t ld_q;
+    float* scales;
+    int64_t ld_s;
+} fp8q_act_tensor;
+
+fp8q_status quantize_act_per_token_group_batched(const fp8q_act_tensor* tensors, int32_t count,
+                                                 int32_t* nonfinite_flag, void* stream);
+
+/*
  * rmsnorm_quantize_act_per_token_group -- SURVEY §8(f) NEXT-2: quantize_act_per_token_group
  * fused into its producer on the rollout forward (the RMSNorm before q/k/v and gate/up):
  *   y[m, j] = BF16_RNE( x[m, j] / sqrt(mean_i x[m, i]^2 + eps) * gamma[j] )   (binary32 inside)

@@ -18,6 +18,7 @@ from .fp8q import (  # noqa: F401
     kv_scale_from_amax,
     load_library,
     quantize_act_per_token_group,
+    quantize_act_per_token_group_batched,
     quantize_weight_blockwise,
     quantize_weight_blockwise_batched,
     rmsnorm_quantize_act_per_token_group,

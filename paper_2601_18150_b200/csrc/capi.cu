@@ -181,6 +181,46 @@ fp8q_status quantize_act_per_token_group(const void* x_bf16, int64_t m, int64_t 
     return from_cuda(e);
 }
 
+static fp8q_status check_act(const void* x_bf16, int64_t m, int64_t k, int64_t ld_x, const uint8_t* codes,
+                             int64_t ld_q, const float* scales, int64_t ld_s) {
+    if (m < 0 || k < 0) return FP8Q_EINVAL;
+    if (ld_x < k || ld_q < k || ld_s < m) return FP8Q_EINVAL;
+    if (k % 128 != 0) return FP8Q_ESHAPE;
+    if (m == 0 || k == 0) return FP8Q_OK;
+    if (x_bf16 == nullptr || codes == nullptr || scales == nullptr) return FP8Q_EINVAL;
+    if (!aligned(x_bf16, 16) || ld_x % 8 != 0 || !aligned(codes, 8) || ld_q % 8 != 0 || !aligned(scales, 4) ||
+        ld_s % 4 != 0)
+        return FP8Q_EALIGN;
+    return FP8Q_OK;
+}
+
+fp8q_status quantize_act_per_token_group_batched(const fp8q_act_tensor* tensors, int32_t count,
+                                                 int32_t* nonfinite_flag, void* stream) {
+    if (count < 0 || (count > 0 && tensors == nullptr)) return FP8Q_EINVAL;
+    if (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)) return FP8Q_EALIGN;
+    for (int32_t i = 0; i < count; ++i) {
+        const fp8q_act_tensor& t = tensors[i];
+        fp8q_status st = check_act(t.x_bf16, t.m, t.k, t.ld_x, t.codes, t.ld_q, t.scales, t.ld_s);
+        if (st != FP8Q_OK) return st;
+    }
+    if (count == 0) return FP8Q_OK;
+    fp8q_status st = check_device();
+    if (st != FP8Q_OK) return st;
+    fp8q::ActDesc d[fp8q::kMaxActBatch];
+    for (int32_t base = 0; base < count; base += fp8q::kMaxActBatch) {
+        const int32_t c = count - base < fp8q::kMaxActBatch ? count - base : fp8q::kMaxActBatch;
+        for (int32_t i = 0; i < c; ++i) {
+            const fp8q_act_tensor& t = tensors[base + i];
+            d[i] = fp8q::ActDesc{static_cast<const uint16_t*>(t.x_bf16), t.m, t.k, t.ld_x, t.codes, t.ld_q,
+                                 t.scales, t.ld_s};
+        }
+        cudaError_t e = fp8q::launch_act_batch(d, c, nonfinite_flag, static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return from_cuda(e);
+        g_launches.fetch_add(fp8q::act_batch_launches(d, c));
+    }
+    return FP8Q_OK;
+}
+
 static fp8q_status check_act_out(int64_t m, int64_t k, const uint8_t* codes, int64_t ld_q, const float* scales,
                                  int64_t ld_s, const void* y, int64_t ld_y, const int32_t* flag) {
     if (ld_q < k || ld_s < m || (y != nullptr && ld_y < k)) return FP8Q_EINVAL;

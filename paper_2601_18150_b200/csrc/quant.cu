@@ -512,24 +512,43 @@ __device__ __forceinline__ void aq_load_smem(uint32_t base, int64_t groups, int6
         }
     }
 }
+// A batch of activation tensors for one launch of the staged kernel (the four GEMM inputs of a
+// layer in one persistent launch: one pipeline ramp and one tail instead of four).  Items are
+// numbered across the batch (tensor i owns items [item0, item0 + m * chunks)).
+struct ATensor {
+    const uint16_t* x;
+    uint8_t* q;
+    float* scales;
+    int64_t ld_x, ld_q, ld_s, groups, m;
+    int32_t chunks;  // 16-group (4 KB) items per token row
+    int64_t item0;   // first batch-global item of this tensor
+};
+struct ABatch {
+    CUtensorMap tm[kMaxActBatch];  // kTma: 3-D map {128 channels, groups, m}, box {128, 16, 1}
+    ATensor t[kMaxActBatch];
+    int count;
+    int64_t items;
+};
 // kTma: each item is ONE 3-D TMA box (128 BF16 x 16 groups x 1 row of the tensor map
 // {128, groups, m}, groups past the row zero-filled) instead of a cp.async.bulk copy; same
 // shared-memory layout, same consumers.
 template <bool kTma>
 __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kernel(
-    const __grid_constant__ CUtensorMap tmx,
-    const uint16_t* __restrict__ x, int64_t ld_x, uint8_t* __restrict__ q, int64_t ld_q,
-    float* __restrict__ scales, int64_t ld_s, int64_t groups, int64_t chunks, int64_t items,
-    int32_t* __restrict__ nonfinite_flag) {
+    const __grid_constant__ ABatch ab, int32_t* __restrict__ nonfinite_flag) {
     extern __shared__ __align__(128) uint8_t abq_smem[];
     __shared__ ScaleTables tabs;
     uint64_t* full = reinterpret_cast<uint64_t*>(abq_smem + size_t(ABQ_STAGES) * ABQ_ITEMS * ABQ_ITEM_BYTES);
     uint64_t* empty = full + ABQ_STAGES;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // this CTA's equal share of the items
-    const int64_t i0 = items * blockIdx.x / gridDim.x;
-    const int64_t i1 = items * (blockIdx.x + 1) / gridDim.x;
+    // this CTA's equal share of the batch's items
+    const int64_t i0 = ab.items * blockIdx.x / gridDim.x;
+    const int64_t i1 = ab.items * (blockIdx.x + 1) / gridDim.x;
     const int64_t nstages = (i1 - i0 + ABQ_ITEMS - 1) / ABQ_ITEMS;
+    auto tensor_of = [&](int64_t item) {
+        int i = 0;
+        while (i + 1 < ab.count && item >= ab.t[i + 1].item0) ++i;
+        return i;
+    };
     init_scale_tables(tabs);
     if (threadIdx.x == 0) {
         for (int s = 0; s < ABQ_STAGES; ++s) {
@@ -541,12 +560,12 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
     __syncthreads();
     const uint32_t ring = smem_u32(abq_smem);
     if (warp == ABQ_ITEMS * ABQ_TEAMS) {
-        if (lane == 0) {
-            // (row, chunk) of the current item, advanced incrementally (no 64-bit division)
-            int64_t row = i0 / chunks;
-            int32_t chunk = static_cast<int32_t>(i0 - row * chunks);
-            const int32_t nch = static_cast<int32_t>(chunks);
-            const uint32_t tail_bytes = static_cast<uint32_t>(groups - (chunks - 1) * 16) * 256u;
+        if (lane == 0 && i1 > i0) {
+            // (tensor, row, chunk) of the current item, advanced incrementally (no 64-bit division
+            // per item)
+            int ti = tensor_of(i0);
+            int64_t row = (i0 - ab.t[ti].item0) / ab.t[ti].chunks;
+            int32_t chunk = static_cast<int32_t>(i0 - ab.t[ti].item0 - row * ab.t[ti].chunks);
             int64_t left = i1 - i0;
             uint32_t s = 0, ph = 0;
             while (left > 0) {
@@ -554,21 +573,27 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
                 const int cnt = left < ABQ_ITEMS ? static_cast<int>(left) : ABQ_ITEMS;
                 uint32_t bytes = 0;
                 for (int j = 0; j < cnt; ++j) {
+                    const ATensor& t = ab.t[ti];
                     // copies may complete before the expect_tx below: the phase cannot, since
                     // its one arrival (the expect_tx arrive) is still pending
                     if (kTma) {
-                        tma_load_3d(abq_smem + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, &tmx, &full[s], 0, chunk * 16,
-                                    static_cast<int32_t>(row));
+                        tma_load_3d(abq_smem + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, &ab.tm[ti], &full[s], 0,
+                                    chunk * 16, static_cast<int32_t>(row));
                         bytes += 4096u;  // the whole box counts, zero-filled groups included
                     } else {
-                        const uint32_t nb = chunk == nch - 1 ? tail_bytes : 4096u;
-                        bulk_g2s(ring + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, x + row * ld_x + chunk * 2048, nb,
-                                 &full[s]);
+                        const uint32_t nb = chunk == t.chunks - 1
+                                                ? static_cast<uint32_t>(t.groups - (t.chunks - 1) * 16) * 256u
+                                                : 4096u;
+                        bulk_g2s(ring + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, t.x + row * t.ld_x + chunk * 2048,
+                                 nb, &full[s]);
                         bytes += nb;
                     }
-                    if (++chunk == nch) {
+                    if (++chunk == t.chunks) {
                         chunk = 0;
-                        ++row;
+                        if (++row == t.m) {
+                            row = 0;
+                            ++ti;
+                        }
                     }
                 }
                 mbar_arrive_expect_tx(&full[s], bytes);
@@ -587,14 +612,16 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
         mbar_wait(&full[s], static_cast<uint32_t>((it / ABQ_STAGES) & 1));
         const int64_t item = i0 + it * ABQ_ITEMS + w;
         if (item < i1) {
-            // 32-bit (the host keeps items < 2^31 on this path): once per 4 KB item
-            const int64_t row = static_cast<uint32_t>(item) / static_cast<uint32_t>(chunks);
-            const int64_t chunk = item - row * chunks;
+            const ATensor& t = ab.t[tensor_of(item)];
+            // 32-bit (the host keeps each tensor's items < 2^31): once per 4 KB item
+            const uint32_t local = static_cast<uint32_t>(item - t.item0);
+            const int64_t row = local / static_cast<uint32_t>(t.chunks);
+            const int64_t chunk = local - row * t.chunks;
             AItemRegs d;
-            aq_load_smem(ring + (s * ABQ_ITEMS + w) * ABQ_ITEM_BYTES, groups, chunk, d);
+            aq_load_smem(ring + (s * ABQ_ITEMS + w) * ABQ_ITEM_BYTES, t.groups, chunk, d);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // the item is in registers: free the slot
-            aq_process(d, q, ld_q, scales, ld_s, groups, row, chunk, nonfinite_flag, tabs);
+            aq_process(d, t.q, t.ld_q, t.scales, t.ld_s, t.groups, row, chunk, nonfinite_flag, tabs);
         } else {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -894,74 +921,137 @@ cudaError_t launch_weight_blockwise(const uint16_t* w, int64_t n, int64_t k, int
     return launch_weight_blockwise_batch(&d, 1, flag, stream);
 }
 
-cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, int64_t ld_x,
-                                       uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
-                                       int32_t* flag, cudaStream_t stream) {
-    const int64_t groups = k / 128;
-    const int64_t chunks = (groups + 7) / 8;
-    const int64_t items = m * chunks;
-    if (items == 0) return cudaSuccess;
-    const int64_t blocks = (items + 7) / 8;
-    if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
-    static const int act_kernel = [] {  // dev: FP8Q_ACT_KERNEL=wide selects the warp-persistent path
+namespace {
+// The staged kernel's requirements: x 16-byte aligned with ld_x % 8 == 0 (TMA / bulk copies),
+// codes 16-byte aligned with ld_q % 16 == 0 (16-byte stores), items < 2^31 per tensor.
+bool act_staged_ok(const ActDesc& d) {
+    const int64_t groups = d.k / 128;
+    return al(d.x, 16) && d.ld_x % 8 == 0 && al(d.q, 16) && d.ld_q % 16 == 0 &&
+           d.m * ((groups + 15) / 16) < (1LL << 31);
+}
+int act_kernel_env() {  // dev: FP8Q_ACT_KERNEL=wide selects the warp-persistent path
+    static const int v = [] {
         const char* e = std::getenv("FP8Q_ACT_KERNEL");
         return (e != nullptr && e[0] == 'w') ? 1 : 0;
     }();
-    if (act_kernel == 0 && al(x, 16) && ld_x % 8 == 0 && al(q, 16) && ld_q % 16 == 0 &&
-        m * ((groups + 15) / 16) < (1LL << 31)) {
-        static bool attr_done[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev >= 0 && dev < 64 && !attr_done[dev]) {
-            cudaError_t ea = cudaFuncSetAttribute(act_per_token_group_bulk_kernel<false>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  static_cast<int>(ABQ_SMEM));
-            if (ea == cudaSuccess)
-                ea = cudaFuncSetAttribute(act_per_token_group_bulk_kernel<true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ABQ_SMEM));
-            if (ea != cudaSuccess) return ea;
-            attr_done[dev] = true;
-        }
-        // dev A/B: FP8Q_ACT_LOAD=bulk keeps the cp.async.bulk copies
-        static const bool act_tma_env = [] {
-            const char* e = std::getenv("FP8Q_ACT_LOAD");
-            return !(e != nullptr && e[0] == 'b');
-        }();
-        const auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encode_fn());
-        CUtensorMap tmx{};
-        bool use_tma = act_tma_env && encode != nullptr;
-        if (use_tma) {
-            cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(groups), static_cast<cuuint64_t>(m)};
-            cuuint64_t strides[2] = {256, static_cast<cuuint64_t>(ld_x) * 2};
-            cuuint32_t box[3] = {128, 16, 1};
-            cuuint32_t estr[3] = {1, 1, 1};
-            use_tma = encode(&tmx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(x), dims, strides, box,
-                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-        }
+    return v;
+}
+
+cudaError_t launch_act_unstaged(const ActDesc& d, int32_t* flag, cudaStream_t stream) {
+    const int64_t groups = d.k / 128;
+    if (al(d.x, 32) && d.ld_x % 16 == 0 && al(d.q, 16) && d.ld_q % 16 == 0) {
         const int64_t wchunks = (groups + 15) / 16;
-        const int64_t witems = m * wchunks;
-        const int64_t per_cta_min = 2 * ABQ_ITEMS;  // small inputs: fewer CTAs, each a few stages
-        int64_t grid = (witems + per_cta_min - 1) / per_cta_min;
-        grid = grid < sm_count() ? grid : sm_count();
-        if (use_tma)
-            act_per_token_group_bulk_kernel<true><<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
-                tmx, x, ld_x, q, ld_q, scales, ld_s, groups, wchunks, witems, flag);
-        else
-            act_per_token_group_bulk_kernel<false><<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
-                tmx, x, ld_x, q, ld_q, scales, ld_s, groups, wchunks, witems, flag);
-    } else if (al(x, 32) && ld_x % 16 == 0 && al(q, 16) && ld_q % 16 == 0) {
-        const int64_t wchunks = (groups + 15) / 16;
-        const int64_t witems = m * wchunks;
+        const int64_t witems = d.m * wchunks;
         const int64_t wblocks = (witems + 7) / 8;
         const int64_t grid = wblocks < 2LL * sm_count() ? wblocks : 2LL * sm_count();
         act_per_token_group_wide_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(
-            x, ld_x, q, ld_q, scales, ld_s, groups, wchunks, witems, flag);
+            d.x, d.ld_x, d.q, d.ld_q, d.scales, d.ld_s, groups, wchunks, witems, flag);
     } else {
+        const int64_t chunks = (groups + 7) / 8;
+        const int64_t blocks = (d.m * chunks + 7) / 8;
+        if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
         act_per_token_group_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-            x, m, k, ld_x, q, ld_q, scales, ld_s, chunks, flag);
+            d.x, d.m, d.k, d.ld_x, d.q, d.ld_q, d.scales, d.ld_s, chunks, flag);
     }
     return cudaGetLastError();
+}
+}  // namespace
+
+int act_batch_launches(const ActDesc* descs, int count) {
+    int staged = 0, other = 0;
+    for (int i = 0; i < count; ++i) {
+        if (descs[i].m == 0 || descs[i].k == 0) continue;
+        if (act_kernel_env() == 0 && act_staged_ok(descs[i])) ++staged; else ++other;
+    }
+    return other + (staged + kMaxActBatch - 1) / kMaxActBatch;
+}
+
+cudaError_t launch_act_batch(const ActDesc* descs, int count, int32_t* flag, cudaStream_t stream) {
+    static bool attr_done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !attr_done[dev]) {
+        cudaError_t ea = cudaFuncSetAttribute(act_per_token_group_bulk_kernel<false>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ABQ_SMEM));
+        if (ea == cudaSuccess)
+            ea = cudaFuncSetAttribute(act_per_token_group_bulk_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ABQ_SMEM));
+        if (ea != cudaSuccess) return ea;
+        attr_done[dev] = true;
+    }
+    // dev A/B: FP8Q_ACT_LOAD=bulk keeps the cp.async.bulk copies
+    static const bool act_tma_env = [] {
+        const char* e = std::getenv("FP8Q_ACT_LOAD");
+        return !(e != nullptr && e[0] == 'b');
+    }();
+    const auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encode_fn());
+    const bool use_tma = act_tma_env && encode != nullptr;
+    ABatch ab{};
+    ab.count = 0;
+    ab.items = 0;
+    auto flush = [&]() -> cudaError_t {
+        if (ab.count == 0 || ab.items == 0) {
+            ab.count = 0;
+            ab.items = 0;
+            return cudaSuccess;
+        }
+        const int64_t per_cta_min = 2 * ABQ_ITEMS;  // small inputs: fewer CTAs, each a few stages
+        int64_t grid = (ab.items + per_cta_min - 1) / per_cta_min;
+        grid = grid < sm_count() ? grid : sm_count();
+        if (use_tma)
+            act_per_token_group_bulk_kernel<true><<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
+                ab, flag);
+        else
+            act_per_token_group_bulk_kernel<false><<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
+                ab, flag);
+        ab.count = 0;
+        ab.items = 0;
+        return cudaGetLastError();
+    };
+    for (int i = 0; i < count; ++i) {
+        const ActDesc& d = descs[i];
+        if (d.m == 0 || d.k == 0) continue;
+        if (act_kernel_env() != 0 || !act_staged_ok(d)) {
+            cudaError_t e = launch_act_unstaged(d, flag, stream);
+            if (e != cudaSuccess) return e;
+            continue;
+        }
+        const int64_t groups = d.k / 128;
+        ATensor& t = ab.t[ab.count];
+        t.x = d.x;
+        t.q = d.q;
+        t.scales = d.scales;
+        t.ld_x = d.ld_x;
+        t.ld_q = d.ld_q;
+        t.ld_s = d.ld_s;
+        t.groups = groups;
+        t.m = d.m;
+        t.chunks = static_cast<int32_t>((groups + 15) / 16);
+        t.item0 = ab.items;
+        if (use_tma) {
+            cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(groups), static_cast<cuuint64_t>(d.m)};
+            cuuint64_t strides[2] = {256, static_cast<cuuint64_t>(d.ld_x) * 2};
+            cuuint32_t box[3] = {128, 16, 1};
+            cuuint32_t estr[3] = {1, 1, 1};
+            if (encode(&ab.tm[ab.count], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(d.x), dims,
+                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return cudaErrorInvalidValue;
+        }
+        ab.items += d.m * t.chunks;
+        if (++ab.count == kMaxActBatch) {
+            cudaError_t e = flush();
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return flush();
+}
+
+cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, int64_t ld_x,
+                                       uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
+                                       int32_t* flag, cudaStream_t stream) {
+    const ActDesc d{x, m, k, ld_x, q, ld_q, scales, ld_s};
+    return launch_act_batch(&d, 1, flag, stream);
 }
 
 }  // namespace fp8q

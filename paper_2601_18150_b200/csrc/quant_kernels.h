@@ -35,6 +35,20 @@ cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, 
                                        uint8_t* q, int64_t ld_q, float* scales, int64_t ld_s,
                                        int32_t* flag, cudaStream_t stream);
 
+// Several activation tensors in as few launches as possible (kMaxActBatch staged-path tensors
+// per persistent launch; tensors that miss the staged path's alignment get their own launch).
+constexpr int kMaxActBatch = 8;
+struct ActDesc {
+    const uint16_t* x;
+    int64_t m, k, ld_x;
+    uint8_t* q;
+    int64_t ld_q;
+    float* scales;
+    int64_t ld_s;
+};
+cudaError_t launch_act_batch(const ActDesc* descs, int count, int32_t* flag, cudaStream_t stream);
+int act_batch_launches(const ActDesc* descs, int count);
+
 struct GemmArgs {
     const uint8_t* a;
     int64_t ld_a;

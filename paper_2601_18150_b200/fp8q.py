@@ -32,6 +32,13 @@ class WeightTensorDesc(ctypes.Structure):
                 ("scales", ctypes.c_void_p), ("ld_s", ctypes.c_int64)]
 
 
+class ActTensorDesc(ctypes.Structure):
+    """fp8q_act_tensor (include/fp8q.h)."""
+    _fields_ = [("x_bf16", ctypes.c_void_p), ("m", ctypes.c_int64), ("k", ctypes.c_int64),
+                ("ld_x", ctypes.c_int64), ("codes", ctypes.c_void_p), ("ld_q", ctypes.c_int64),
+                ("scales", ctypes.c_void_p), ("ld_s", ctypes.c_int64)]
+
+
 class Fp8qError(RuntimeError):
     """A libfp8q entry point returned a non-OK fp8q_status."""
 
@@ -62,6 +69,8 @@ def load_library() -> ctypes.CDLL:
         lib.e4m3_encode_f32.restype = ctypes.c_int
         lib.quantize_act_per_token_group.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
         lib.quantize_act_per_token_group.restype = ctypes.c_int
+        lib.quantize_act_per_token_group_batched.argtypes = [ctypes.POINTER(ActTensorDesc), I32, P, P]
+        lib.quantize_act_per_token_group_batched.restype = ctypes.c_int
         lib.rmsnorm_quantize_act_per_token_group.argtypes = [P, P, ctypes.c_float, I64, I64, I64, P, I64, P, I64,
                                                              P, I64, P, P]
         lib.rmsnorm_quantize_act_per_token_group.restype = ctypes.c_int
@@ -239,6 +248,27 @@ def quantize_act_per_token_group(x: torch.Tensor, codes: torch.Tensor | None = N
         scales.stride(0) if scales.shape[0] > 1 else scales.shape[1], flag, _stream(stream)),
         "quantize_act_per_token_group")
     return codes, scales
+
+
+def quantize_act_per_token_group_batched(items, nonfinite_flag: torch.Tensor | None = None, stream=None):
+    """Several dynamic activation quantizations in as few launches as
+    possible -- a layer's GEMM inputs in one persistent launch.  items: sequence of
+    (x, codes, scales) CUDA tensors with the shapes of quantize_act_per_token_group's
+    inputs/outputs (scales MN-major [k/128, >= m])."""
+    items = list(items)
+    arr = (ActTensorDesc * max(1, len(items)))()
+    for i, (x, codes, scales) in enumerate(items):
+        _cuda2d(x, "x", torch.bfloat16)
+        _cuda2d(codes, "codes", torch.uint8)
+        _cuda2d(scales, "scales", torch.float32)
+        m, k = x.shape
+        if codes.shape != (m, k) or scales.shape[0] < k // 128 or scales.shape[1] < m:
+            raise Fp8qError(f"item {i}: output shape mismatch")
+        arr[i] = ActTensorDesc(x.data_ptr(), m, k, _ld(x), codes.data_ptr(), _ld(codes), scales.data_ptr(),
+                               scales.stride(0) if scales.shape[0] > 1 else scales.shape[1])
+    flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
+    _check(load_library().quantize_act_per_token_group_batched(arr, len(items), flag, _stream(stream)),
+           "quantize_act_per_token_group_batched")
 
 
 def _act_outputs(m, k, device, codes, scales):

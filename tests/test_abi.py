@@ -35,7 +35,7 @@ def test_header_declares_the_boundary():
                      "fp8q_kernel_launches", "rmsnorm_quantize_act_per_token_group",
                      "silu_mul_quantize_act_per_token_group", "kv_amax_update", "kv_scale_from_amax",
                      "kv_quantize_append", "quantize_weight_blockwise_fanout", "mx_scale_bytes", "mx_quantize",
-                     "fp8_mx_gemm"]:
+                     "fp8_mx_gemm", "quantize_act_per_token_group_batched", "quantize_weight_blockwise_batched"]:
         assert required in names
 
 
@@ -68,6 +68,15 @@ def test_validation_paths_without_gpu(lib):
     # activations: k % 128 -> ESHAPE, ld_s % 4 -> EALIGN
     assert lib.quantize_act_per_token_group(fake, 4, 200, 200, fake, 200, fake, 4, None, None) == 2
     assert lib.quantize_act_per_token_group(fake, 3, 128, 128, fake, 128, fake, 3, None, None) == 3
+    # batched activations: every descriptor is validated first (second one bad -> its status)
+    from paper_2601_18150_b200.fp8q import ActTensorDesc
+    arr = (ActTensorDesc * 2)(ActTensorDesc(0x10000, 4, 128, 128, 0x10000, 128, 0x10000, 4),
+                              ActTensorDesc(0x10000, 4, 200, 200, 0x10000, 200, 0x10000, 4))
+    assert lib.quantize_act_per_token_group_batched(arr, 2, None, None) == 2
+    arr[1] = ActTensorDesc(0x10001, 4, 128, 128, 0x10000, 128, 0x10000, 4)
+    assert lib.quantize_act_per_token_group_batched(arr, 2, None, None) == 3
+    assert lib.quantize_act_per_token_group_batched(arr, -1, None, None) == 1
+    assert lib.quantize_act_per_token_group_batched(None, 0, None, None) == 0
     # GEMM: n % 8 -> ESHAPE; k % 128 -> ESHAPE; misaligned ld_a -> EALIGN
     assert lib.fp8_block_gemm(fake, 128, fake, 4, fake, 128, fake, 1, fake, 12, 0, 4, 12, 128, None, 0, None) == 2
     assert lib.fp8_block_gemm(fake, 200, fake, 4, fake, 200, fake, 1, fake, 16, 0, 4, 16, 200, None, 0, None) == 2

@@ -249,3 +249,60 @@ def test_weight_forced_path_ragged(path):
     r = subprocess.run([sys.executable, "-c", _BULK_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "bulk ok" in r.stdout, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ batched activation launch
+@pytest.mark.parametrize("shapes", [
+    # a Qwen3-8B layer's four GEMM inputs (K = 4096 x 3, 12288) at a ragged token count
+    [(300, 4096), (300, 4096), (300, 4096), (300, 12288)],
+    # groups not a multiple of 16 (zero-filled tail items), one-row and empty tensors mixed in
+    [(5, 384), (1, 128), (0, 256), (33, 2176), (130, 1024)],
+    # more tensors than one launch takes (8): split over two launches
+    [(17 + i, 128 * (i + 1)) for i in range(11)],
+])
+def test_act_batched_matches_oracle(shapes):
+    items, ref = [], []
+    for i, (m, k) in enumerate(shapes):
+        bits = synth.qwen3_activation(m, k, seed=500 + i)
+        x = to_dev_bf16(bits) if m else torch.empty((0, k), dtype=torch.bfloat16, device="cuda")
+        codes = torch.full((m, k), 0xAB, dtype=torch.uint8, device="cuda")
+        scales = torch.full((k // 128, fp8q.act_scales_ld(m)), -1.0, dtype=torch.float32, device="cuda")
+        items.append((x, codes, scales))
+        ref.append(oracle.quantize_act_per_token_group(bits) if m else None)
+    before = fp8q.kernel_launches()
+    fp8q.quantize_act_per_token_group_batched(items)
+    torch.cuda.synchronize()
+    assert fp8q.kernel_launches() - before == (len([s for s in shapes if s[0]]) + 7) // 8
+    for (m, k), (x, codes, scales), r in zip(shapes, items, ref):
+        if not m:
+            continue
+        oc, os_ = r
+        assert np.array_equal(to_host_u8(codes), oc), (m, k)
+        assert np.array_equal(act_scales_logical(scales, m).view(np.uint32), os_.view(np.uint32)), (m, k)
+
+
+def test_act_batched_equals_single_calls_full_size():
+    # the bench step's inputs: [8192, 4096] x 3 + [8192, 12288] in one launch == four launches
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    items_b, items_s = [], []
+    for k in (4096, 4096, 4096, 12288):
+        x = torch.randn((8192, k), generator=g, device="cuda").to(torch.bfloat16)
+        x[:, ::997] *= 50
+        for lst in (items_b, items_s):
+            lst.append((x, torch.empty((8192, k), dtype=torch.uint8, device="cuda"),
+                        torch.empty((k // 128, 8192), dtype=torch.float32, device="cuda")))
+    fp8q.quantize_act_per_token_group_batched(items_b)
+    for x, c, s in items_s:
+        fp8q.quantize_act_per_token_group(x, c, s)
+    torch.cuda.synchronize()
+    for (_, cb, sb), (_, cs, ss) in zip(items_b, items_s):
+        assert torch.equal(cb, cs)
+        assert torch.equal(sb.view(torch.int32), ss.view(torch.int32))
+    # and a sampled slice of the batch against the oracle (rows spread over the whole range)
+    x, c, s = items_b[3]
+    rows = torch.arange(0, 8192, 401)
+    bits = x[rows].view(torch.int16).cpu().numpy().view(np.uint16)
+    oc, os_ = oracle.quantize_act_per_token_group(bits)
+    assert np.array_equal(to_host_u8(c[rows]), oc)
+    assert np.array_equal(to_host_f32(s[:, rows]).T.view(np.uint32), os_.view(np.uint32))
