@@ -6,8 +6,9 @@ The product package ``paper_2601_18150_b200`` never imports it, and this package
 imports nothing from the product package: the two share no code.
 
 Every function is a thin ctypes marshaller around ``fp8q_oracle.c`` (plain C,
-binary32 where the DESIGN.md readings fix binary32, binary64 for the GEMM); the
-arithmetic and its citations live in that file.  Parity pins: ``tests/test_oracle_*.py``.
+binary32 where the DESIGN.md readings fix binary32, binary64 for the GEMM), except the NEXT-2
+producers, which are plain Python (integers, fractions, decimal, numpy binary32) in
+``producers.py``; the arithmetic and its citations live in those files.  Parity pins: ``tests/test_oracle_*.py``.
 No function here is "parity unpinned" (see DESIGN.md §3.3 for the pin of each one).
 """
 from __future__ import annotations
@@ -18,6 +19,8 @@ import subprocess
 import threading
 
 import numpy as np
+
+from . import producers as _producers
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "fp8q_oracle.c")
@@ -62,10 +65,6 @@ def _load():
             lib.oracle_gemm_rows.restype = ctypes.c_int
             lib.oracle_f64_to_bf16.argtypes = [ctypes.c_double]
             lib.oracle_f64_to_bf16.restype = ctypes.c_uint16
-            lib.oracle_rmsnorm_bf16.argtypes = [P, I64, I64, P, ctypes.c_double, P]
-            lib.oracle_rmsnorm_bf16.restype = None
-            lib.oracle_silu_mul_bf16.argtypes = [P, I64, I64, P]
-            lib.oracle_silu_mul_bf16.restype = None
             lib.oracle_kv_amax.argtypes = [P, I64, I64, I64, P]
             lib.oracle_kv_amax.restype = ctypes.c_int
             lib.oracle_kv_quantize_append.argtypes = [P, I64, I64, I64, ctypes.c_float, P, P, I64]
@@ -221,26 +220,29 @@ def f64_to_bf16(d: float) -> int:
 
 
 def rmsnorm_bf16(x_bits: np.ndarray, gamma_bits: np.ndarray, eps: float) -> np.ndarray:
-    """y = BF16_RNE(x / sqrt(mean(x^2) + eps) * gamma), binary64 inside."""
+    """NEXT-2 RMSNorm (reading N2; oracle/producers.py): Qwen3RMSNorm with every
+    binary32 step correctly rounded and the sum of squares exact, rounded to BF16 twice."""
     x = _as_bf16_bits(x_bits)
     g = _as_bf16_bits(gamma_bits)
     m, k = x.shape
     if g.shape != (k,):
         raise OracleError("gamma must have shape [k]")
-    y = np.empty((m, k), dtype=np.uint16)
-    _load().oracle_rmsnorm_bf16(_ptr(x), m, k, _ptr(g), float(eps), _ptr(y))
-    return y
+    return _producers.rmsnorm_bf16(x, g, eps)
 
 
 def silu_mul_bf16(gate_up_bits: np.ndarray) -> np.ndarray:
-    """y = BF16_RNE(silu(gate) * up) for gate_up = [gate | up] (each [m, I]), binary64 inside."""
+    """NEXT-2 SiLU-mul (reading N2): y = RN_BF16(RN32(RN_BF16(silu(gate)) * up)) for
+    gate_up = [gate | up] (each [m, I]), silu correctly rounded from its real value."""
     gu = _as_bf16_bits(gate_up_bits)
     m, k2 = gu.shape
     if k2 % 2:
         raise OracleError("gate_up must have an even number of columns")
-    y = np.empty((m, k2 // 2), dtype=np.uint16)
-    _load().oracle_silu_mul_bf16(_ptr(gu), m, k2 // 2, _ptr(y))
-    return y
+    return _producers.silu_mul_bf16(gu)
+
+
+def silu_bf16_table() -> np.ndarray:
+    """RN_BF16(silu(g)) for every BF16 bit pattern g (65,536 entries; NaN for non-finite g)."""
+    return _producers.silu_bf16_table()
 
 
 def rmsnorm_quantize(x_bits, gamma_bits, eps, nthreads=None):

@@ -337,10 +337,9 @@ int oracle_gemm_rows(const uint8_t* a, int64_t ld_a, const float* sa, int64_t ld
  * the activation quantizer's producers on the Qwen3 rollout forward,
  * RMSNorm (input of qkv and gate_up) and SiLU(gate) * up (input of down_proj).  The
  * unfused pipeline materialises the producer's output in BF16 and then quantizes it
- * (PAPER.md:65,73), so the oracle's definition is:  y = BF16_RNE(f(x)) with f evaluated in
- * binary64, then O3-O6 per-token-group quantization of y.
- *   RMSNorm:   f(x)_j = x_j / sqrt(mean_i(x_i^2) + eps) * gamma_j
- *   SiLU-mul:  f(g, u) = g / (1 + exp(-g)) * u
+ * (PAPER.md:65,73).  The producers themselves (readings N1, N2) live in oracle/producers.py
+ * (exact integer / rational / decimal arithmetic); this file keeps the binary64 -> BF16
+ * rounding helper.
  */
 
 /* binary64 -> BF16 bits, round to nearest even (direct: no double rounding through fp32). */
@@ -362,36 +361,6 @@ uint16_t oracle_f64_to_bf16(double d) {
     uint32_t u;
     memcpy(&u, &f, 4);
     return sign | (uint16_t)((u >> 16) & 0x7FFF);
-}
-
-void oracle_rmsnorm_bf16(const uint16_t* x, int64_t m, int64_t k, const uint16_t* gamma, double eps,
-                         uint16_t* y) {
-    for (int64_t r = 0; r < m; ++r) {
-        double ss = 0.0;
-        for (int64_t j = 0; j < k; ++j) {
-            double v = (double)oracle_bf16_to_float(x[r * k + j]);
-            ss += v * v;
-        }
-        double inv = 1.0 / sqrt(ss / (double)k + eps);
-        for (int64_t j = 0; j < k; ++j) {
-            double v = (double)oracle_bf16_to_float(x[r * k + j]);
-            double gj = (double)oracle_bf16_to_float(gamma[j]);
-            y[r * k + j] = oracle_f64_to_bf16(v * inv * gj);
-        }
-    }
-}
-
-void oracle_silu_mul_bf16(const uint16_t* gate_up, int64_t m, int64_t inter, uint16_t* y) {
-    for (int64_t r = 0; r < m; ++r) {
-        const uint16_t* g = gate_up + r * 2 * inter;
-        const uint16_t* u = g + inter;
-        for (int64_t j = 0; j < inter; ++j) {
-            double gv = (double)oracle_bf16_to_float(g[j]);
-            double uv = (double)oracle_bf16_to_float(u[j]);
-            double silu = gv / (1.0 + exp(-gv));
-            y[r * inter + j] = oracle_f64_to_bf16(silu * uv);
-        }
-    }
 }
 
 /* ================================================================== NEXT-3: FP8 KV cache
