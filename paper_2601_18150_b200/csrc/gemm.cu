@@ -95,23 +95,8 @@ struct KParams {
     int raster;              // m-tiles per raster band (TileCursor)
     float* ws;               // split-K partials [tile][split][128][BN] fp32
     int32_t* counters;       // split-K arrival counters [tile], zero between launches
-    uint32_t* trace;         // dev-only timeline (fp8q_debug_set_trace), nullptr in production
-    int debug_mode;          // dev-only: 1 = promotion skips TMEM loads + FMAs (MMA pipe ceiling),
-                             // 2 = also no TMA after the first stages (tensor-core-only ceiling),
-                             // 3 = (pair) the MMA issuer ignores TMEM buffer releases and the
-                             //     promotion/store warps idle: TMA + MMA without the release chain,
-                             // 4 = promotion reads TMEM (all chunks) but does no FMAs,
-                             // 5 = mode 1 without the tile epilogue (no BF16 parking / stores)
     int groups;
 };
-
-// Dev-only timeline: CTA 0 records clock() at pipeline events of its first TRACE_KB k-blocks.
-constexpr int TRACE_KB = 96;
-constexpr int TRACE_EV = 12;
-__device__ __forceinline__ void trace_ev(const KParams& p, uint32_t it, int ev) {
-    if (p.trace != nullptr && blockIdx.x == 0 && it < TRACE_KB)
-        p.trace[it * TRACE_EV + ev] = static_cast<uint32_t>(clock64());
-}
 
 // Walks the (group, m-tile, n-tile) sequence; t must increase between calls.  TM = rows per
 // tile (128 for one CTA, 256 for a CTA pair), GM = m-tiles per raster band.
@@ -235,10 +220,7 @@ __device__ __forceinline__ int split_begin(const KParams& p, int s) {
 // For every k-block: wait for the partial in TMEM buffer it % NBUF, tcgen05.ld it, hand the
 // buffer back (to the leader CTA of a pair when PAIR), and
 // acc += P_kb * (sa[kb][row] * sb[col0/128][kb]) with packed FFMA2; then store the tile.
-// SPLIT (CTA pair only): the partial of k-block `it` arrives as two 128-column slots, one per
-// column half h, in a ring of NBUF slots: slot 2*it + h.  Each half's promotion warps wait
-// only for their own half's MMAs and release only their slot.
-template <int BN, int NBUF, bool PAIR, bool SPLIT = false>
+template <int BN, int NBUF, bool PAIR>
 __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap* tmD, uint8_t* stg,
                                              const EpiTile& tile, const ScalePre& pre, bool has_next,
                                              const EpiTile& next, ScalePre& next_pre, uint32_t tmem,
@@ -248,7 +230,6 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
     constexpr int EPI_COLS = BN / 2;
     constexpr int CHUNKS = EPI_COLS / 32;  // tcgen05.ld 32x32b.x32 per promotion thread
     static_assert(EPI_COLS / 32 <= EPI_CHUNKS, "BF16 row segment must fit the staging chunks");
-    if (threadIdx.x == EPI_WARP0 * 32) trace_ev(p, it, 4);  // dev timeline: tile entry
     const int64_t row = tile.row;
     const int64_t row_end = tile.row_end;
     const int64_t col0 = tile.col0;
@@ -273,48 +254,11 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
             sb1 = __ldg(sbp + kb + 2);
         }
         if (kb == (kb1 - kb0 > 4 ? kb1 - 4 : kb0)) next_pre = load_scales(nq);
-        const uint32_t slot = SPLIT ? 2u * it + static_cast<uint32_t>(h) : it;
-        const uint32_t buf = slot % NBUF;
-        const uint32_t bph = (slot / NBUF) & 1u;
+        const uint32_t buf = it % NBUF;
+        const uint32_t bph = (it / NBUF) & 1u;
         mbar_wait(&tfull[buf], bph);
         tc_fence_after();
-        const bool tr = (threadIdx.x == EPI_WARP0 * 32);
-        if (tr) trace_ev(p, it, 3);
-        const bool tr_last = (threadIdx.x == (EPI_WARP0 + NUM_EPI_WARPS - 1) * 32);
-        if (p.debug_mode >= 1) {
-            if (tr_last) trace_ev(p, it, 9);  // dev: the last promotion warp sees the partial
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (PAIR)
-                    mbar_arrive_cluster(&tempty[buf], 0);
-                else
-                    mbar_arrive(&tempty[buf]);
-            }
-            if (tr) trace_ev(p, it, 8);        // dev: first warp released
-            if (tr_last) trace_ev(p, it, 10);  // dev: last warp released
-            continue;
-        }
-        const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) +
-                               (SPLIT ? buf * EPI_COLS : buf * BN + h * EPI_COLS);
-        if (p.debug_mode == 4) {  // dev: the TMEM read-out alone (no FMAs), then release
-            float v[32];
-#pragma unroll
-            for (int c = 0; c < CHUNKS; ++c) {
-                tmem_ld_32x32b_x32(taddr + c * 32, v);
-                tmem_wait_ld();
-                acc[0].x += v[0] * 0.0f;  // keep the loads live
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (PAIR)
-                    mbar_arrive_cluster(&tempty[buf], 0);
-                else
-                    mbar_arrive(&tempty[buf]);
-            }
-            continue;
-        }
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(qd * 32) << 16) + buf * BN + h * EPI_COLS;
         // Software-pipelined: the tcgen05.ld of chunk c+1 is in flight while chunk c's FMAs
         // issue, so each TMEM load latency after the first overlaps useful work.
         float v[2][32];
@@ -338,11 +282,7 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
                 }
             }
         }
-        if (tr) trace_ev(p, it, 5);
     }
-    const bool tr_store = (threadIdx.x == EPI_WARP0 * 32);
-    if (tr_store) trace_ev(p, it - 1, 6);
-    if (p.debug_mode == 5) return;  // dev: mode 1 without the tile epilogue
     if (!PAIR && p.splits > 1) {
         // ---- split-K: park this slice's fp32 partial; the last slice to arrive sums all
         // slices in slice order (deterministic) and stores the tile.
@@ -414,7 +354,6 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&stg_full[h]);  // release: the staging writes above
-        if (tr_store) trace_ev(p, it - 1, 7);
         return;
     }
     const uint32_t swz = static_cast<uint32_t>((lane >> 1) & 3);
@@ -483,7 +422,6 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
             drain((col0 + pass * PASS_COLS) * 2, 2, std::integral_constant<int, CH>{});
         }
     }
-    if (tr_store) trace_ev(p, it - 1, 7);
 }
 
 // Store warp (warps 2 and 3, otherwise idle): for every tile, wait until the 4 promotion
@@ -586,9 +524,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = split_begin(p, sp); kb < split_begin(p, sp + 1); ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
-                    if (p.debug_mode == 2 && it >= STAGES) break;  // dev: operands stay resident
                     mbar_wait(&empty[stage], ph ^ 1u);
-                    trace_ev(p, it, 0);
                     mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
                     tma_load_2d(smA + stage * A_TILE, &tmA, &full[stage], kb * BK, arow);
                     tma_load_3d(smB + stage * C::B_TILE, &tmB, &full[stage], kb * BK, brow, cur.g);
@@ -612,11 +548,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t ph = (it / STAGES) & 1u;
                     const uint32_t buf = it % NBUF;
                     const uint32_t bph = (it / NBUF) & 1u;
-                    trace_ev(p, it, 11);  // dev: issuer starts waiting for the buffer
                     mbar_wait(&tempty[buf], bph ^ 1u);  // promotion warps drained this buffer
-                    trace_ev(p, it, 1);
-                    if (p.debug_mode != 2 || it < STAGES) mbar_wait(&full[stage], ph);  // TMA landed A and B
-                    trace_ev(p, it, 2);
+                    mbar_wait(&full[stage], ph);        // TMA landed A and B
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(smA + stage * A_TILE);
                     const uint32_t b0 = smem_u32(smB + stage * C::B_TILE);
@@ -703,31 +636,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // leader (both CTAs' TMA bytes + the peer's arrival land there); empty[s] and tfull[b] are
 // arrived in both CTAs by a multicast tcgen05.commit; tempty[b] lives in the leader and
 // collects the 16 promotion warps of the pair.
-// SPLIT: the tile's k-block is issued as two N = PBN/2 MMA groups, one per column half, each
-// committed to its own TMEM slot (NBUF slots of PBN/2 columns), so a half's promotion warps
-// start reading after half the MMA time and the tensor core can run up to NBUF-1 slots ahead
-// of the slowest reader.  Each CTA then holds, per half, PBN/4 B rows: CTA r loads rows
-// [h*PBN/2 + r*PBN/4, +PBN/4) of the tile into its smem half h, so the N = PBN/2 pair MMA
-// (first PBN/4 rows from the leader, next PBN/4 from the peer) covers columns h*PBN/2.. in order.
-template <int PBN, bool SPLIT = false>
+// (Round 1 also measured a 256 x 128 pair tile with four TMEM buffers and a 256 x 256 tile
+// committed per 128-column half: both slower -- an N = 128 pair MMA takes as long as N = 256 --
+// and removed in round 2.)
+template <int PBN>
 struct PairCfg {
     static constexpr int BN = PBN;          // tile columns
     static constexpr int B_HALF = PBN / 2;  // B rows loaded by each CTA
-    static constexpr int B_BOX = SPLIT ? PBN / 4 : PBN / 2;  // B rows per TMA box
+    static constexpr int B_BOX = PBN / 2;   // B rows per TMA box
     static constexpr int STAGE_BYTES = A_TILE + B_HALF * BK;  // per CTA
     static constexpr int STAGES = SMEM_BUDGET / STAGE_BYTES;
-    static constexpr int NBUF = SPLIT ? TMEM_COLS / (PBN / 2) : TMEM_COLS / PBN;
-    static constexpr uint32_t IDESC = idesc_e4m3_f32(2 * BM, SPLIT ? PBN / 2 : PBN);
+    static constexpr int NBUF = TMEM_COLS / PBN;
+    static constexpr uint32_t IDESC = idesc_e4m3_f32(2 * BM, PBN);
     static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * STAGE_BYTES + EPI_STAGE_BYTES + 512;
 };
 constexpr int PAIR_RASTER_GM = 8;  // pair m-tiles (256 rows) per raster band
 
-template <int PBN, bool SPLIT = false>
+template <int PBN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     fp8_block_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                                const __grid_constant__ CUtensorMap tmB,
                                const __grid_constant__ CUtensorMap tmD, const KParams p) {
-    using PC = PairCfg<PBN, SPLIT>;
+    using PC = PairCfg<PBN>;
     constexpr int STAGES = PC::STAGES;
     constexpr int NBUF = PC::NBUF;
     constexpr int PAIR_BN = PC::BN;
@@ -763,9 +693,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);                  // multicast commit
-            // leader: the promotion warps of both CTAs (SPLIT: of one column half).  (Funnelling the
-            // peer's 8 releases through one forwarded remote arrive was measured: no change.)
-            mbar_init(&tempty[b], SPLIT ? NUM_EPI_WARPS : 2 * NUM_EPI_WARPS);
+            // leader: the promotion warps of both CTAs.  (Funnelling the peer's 8 releases
+            // through one forwarded remote arrive was measured: no change.)
+            mbar_init(&tempty[b], 2 * NUM_EPI_WARPS);
         }
         for (int hh = 0; hh < 2; ++hh) {
             mbar_init(&stg_full[hh], 4);
@@ -796,22 +726,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
-                    if (p.debug_mode == 2 && it >= STAGES) continue;  // dev: operands stay resident
                     mbar_wait(&empty[stage], ph ^ 1u);
-                    trace_ev(p, it, 0);
                     if (leader)
                         mbar_arrive_expect_tx(&full[stage], 2 * PAIR_STAGE_BYTES);
                     else
                         mbar_arrive_cluster(&full[stage], 0);
                     tma_load_2d_pair(smA + stage * A_TILE, &tmA, &full[stage], kb * BK, arow);
-                    if (SPLIT) {
-                        const int32_t b0 = nt * PAIR_BN + static_cast<int32_t>(rank) * PC::B_BOX;
-                        tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK), &tmB, &full[stage], kb * BK, b0, cur.g);
-                        tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK) + PC::B_BOX * BK, &tmB, &full[stage],
-                                         kb * BK, b0 + PAIR_BN / 2, cur.g);
-                    } else {
-                        tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK), &tmB, &full[stage], kb * BK, brow, cur.g);
-                    }
+                    tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK), &tmB, &full[stage], kb * BK, brow, cur.g);
                 }
             }
         }
@@ -827,36 +748,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
-                    if (SPLIT) {
-                        mbar_wait(&full[stage], ph);
-                        tc_fence_after();
-                        const uint32_t a0 = smem_u32(smA + stage * A_TILE);
-                        const uint32_t b0 = smem_u32(smB + stage * (PAIR_B_HALF * BK));
-#pragma unroll
-                        for (int hh = 0; hh < 2; ++hh) {
-                            const uint32_t slot = 2u * it + hh;
-                            const uint32_t buf = slot % NBUF;
-                            mbar_wait(&tempty[buf], ((slot / NBUF) & 1u) ^ 1u);
-                            tc_fence_after();
-                            if (hh == 0) trace_ev(p, it, 1);
-                            const uint32_t d = tmem + buf * (PAIR_BN / 2);
-                            const uint32_t bh = b0 + hh * (PC::B_BOX * BK);
-#pragma unroll
-                            for (int kk = 0; kk < BK / 32; ++kk)
-                                mma_f8f6f4_pair(d, smem_desc_k_sw128(a0 + kk * 32), smem_desc_k_sw128(bh + kk * 32),
-                                                PAIR_IDESC, kk > 0 ? 1u : 0u);
-                            mma_commit_pair(&tfull[buf], 0x3);
-                        }
-                        mma_commit_pair(&empty[stage], 0x3);
-                        continue;
-                    }
                     const uint32_t buf = it % NBUF;
                     const uint32_t bph = (it / NBUF) & 1u;
-                    trace_ev(p, it, 11);  // dev: issuer starts waiting for the buffer
-                    if (p.debug_mode != 3) mbar_wait(&tempty[buf], bph ^ 1u);  // dev 3: no release chain
-                    trace_ev(p, it, 1);
-                    if (p.debug_mode != 2 || it < STAGES) mbar_wait(&full[stage], ph);  // dev 2: no TMA
-                    trace_ev(p, it, 2);
+                    mbar_wait(&tempty[buf], bph ^ 1u);  // both CTAs' promotion warps drained it
+                    mbar_wait(&full[stage], ph);        // both CTAs' TMA bytes landed
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(smA + stage * A_TILE);
                     const uint32_t b0 = smem_u32(smB + stage * (PAIR_B_HALF * BK));
@@ -870,21 +765,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             // the peer's last remote arrivals must land before the barriers go away
-            const uint32_t slots = SPLIT ? 2u * it : it;
-            if (p.debug_mode == 3 && slots > 0) {  // dev 3: nobody releases; wait for the last MMAs
-                mbar_wait(&tfull[(slots - 1) % NBUF], ((slots - 1) / NBUF) & 1u);
-            }
-            for (uint32_t j = 0; j < NBUF && j < slots && p.debug_mode != 3; ++j) {
-                const uint32_t i = slots - 1 - j;
+            for (uint32_t j = 0; j < NBUF && j < it; ++j) {
+                const uint32_t i = it - 1 - j;
                 mbar_wait(&tempty[i % NBUF], (i / NBUF) & 1u);
             }
         }
-    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128 && p.debug_mode != 3 &&
-               p.debug_mode != 5) {
+    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128) {
         // ------------------------------------------------------------ store warps (BF16)
-        // (only where promote_tile parks BF16 slices for them: 128 columns per half; with
-        // PBN = 128 the promotion warps store their tile themselves -- gating on out_f32 alone
-        // left these warps waiting for slices that never come, a hang of dev kind 1128)
+        // (only where promote_tile parks BF16 slices for them: 128 columns per half)
         const int h = warp - 2;
         TileCursor<2 * BM, PAIR_RASTER_GM> cur;
         cur.init(p);
@@ -896,7 +784,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             store_tile_half(p, smEpi, h, lane, cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM,
                             int64_t(cur.row0) + cur.rows, col0, stg_full, stg_empty, tile_no);
         }
-    } else if (warp >= EPI_WARP0 && p.debug_mode != 3) {  // dev 3: promotion warps idle
+    } else if (warp >= EPI_WARP0) {
         // ---------------------------------------------------------------- promotion warps
         regs_inc<REGS_EPI>();
         const int h = (warp - EPI_WARP0) >> 2;
@@ -924,7 +812,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const bool have_next = cur.seek(p, tn, mt, nt);
             const EpiTile next = have_next ? make_tile(mt, nt) : tile;
             ScalePre next_pre = pre;
-            promote_tile<PAIR_BN, NBUF, true, SPLIT>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd,
+            promote_tile<PAIR_BN, NBUF, true>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd,
                                               h, lane, tfull, tempty, it, stg_full, stg_empty, tile_no);
             tile = next;
             pre = next_pre;
@@ -976,20 +864,11 @@ cudaError_t device_info(int& sms) {
     if (!di.attr_set) {
         e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(fp8_block_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(Cfg<128>::SMEM_BYTES));
-        if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(fp8_block_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(Cfg<256>::SMEM_BYTES));
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(fp8_block_gemm_pair_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(PairCfg<256>::SMEM_BYTES));
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(fp8_block_gemm_pair_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(PairCfg<128>::SMEM_BYTES));
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(fp8_block_gemm_pair_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(PairCfg<256, true>::SMEM_BYTES));
         if (e != cudaSuccess) return e;
         di.attr_set = true;
     }
@@ -1027,14 +906,14 @@ size_t split_ws_bytes(int64_t m, int64_t n, int sp) {
     return SPLIT_COUNTER_BYTES + static_cast<size_t>(tiles * sp * BM * 256) * 4;
 }
 
-// Kernel choice (see launch_cfg): env FP8Q_GEMM_KIND = 128 | 256 | 1128 | 1256 overrides (dev only).
+// Kernel choice (see launch_cfg): env FP8Q_GEMM_KIND = 256 | 1256 overrides (dev only).
 // Default: the CTA-pair kernel for dense M >= 256, the one-CTA 128 x 256 kernel otherwise.
 int choose_kind(const GemmArgs& a) {
     static int forced = [] {
         const char* e = std::getenv("FP8Q_GEMM_KIND");
         return e ? std::atoi(e) : 0;
     }();
-    if (forced == 128 || forced == 256 || forced == 1128 || forced == 1256 || forced == 2256) return forced;
+    if (forced == 256 || forced == 1256) return forced;
     // Measured (tools/kernel_bench.py --moe, Qwen3-30B-A3B experts): the grouped GEMM's short
     // per-expert k-loops (fc2: 6 k-blocks) and ragged segments favour the one-CTA 128 x 256
     // tile (+5 % at T = 8192, +34-41 % at T = 1024) over the CTA pair.
@@ -1043,15 +922,13 @@ int choose_kind(const GemmArgs& a) {
     return 1256;
 }
 
-// kind: 128 / 256 = one-CTA kernel with that BN; 1128 / 1256 = CTA-pair kernel, 256 x BN tiles;
-// 2256 = CTA-pair kernel, 256 x 256 tiles committed per 128-column half (PairCfg SPLIT).
+// kind: 256 = one-CTA kernel, 128 x 256 tiles; 1256 = CTA-pair kernel, 256 x 256 tiles.
 template <int KIND>
 cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encode, int sms,
                        cudaStream_t stream) {
     constexpr bool kPair = KIND > 1000;
-    constexpr bool kSplit = KIND > 2000;
-    constexpr int BN = kSplit ? KIND - 2000 : (kPair ? KIND - 1000 : KIND);
-    constexpr int B_BOX = kSplit ? BN / 4 : (kPair ? BN / 2 : KIND);
+    constexpr int BN = kPair ? KIND - 1000 : KIND;
+    constexpr int B_BOX = kPair ? BN / 2 : KIND;
     CUtensorMap tmA, tmB;
     {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.m)};
@@ -1092,12 +969,6 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
     KParams p;
-    p.trace = g_trace;
-    static const int debug_mode = [] {
-        const char* e = std::getenv("FP8Q_GEMM_DEBUG");
-        return e ? std::atoi(e) : 0;
-    }();
-    p.debug_mode = debug_mode;
     p.sa = a.sa;
     p.ld_sa = a.ld_sa;
     p.sb = a.sb;
@@ -1145,8 +1016,8 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
             const int64_t tiles = ((a.m + 2 * BM - 1) / (2 * BM)) * p.num_n_tiles;
             clusters = tiles < clusters ? tiles : clusters;
         }
-        fp8_block_gemm_pair_kernel<BN, kSplit><<<static_cast<unsigned>(2 * clusters), NUM_THREADS,
-                                                 PairCfg<BN, kSplit>::SMEM_BYTES, stream>>>(tmA, tmB, tmD, p);
+        fp8_block_gemm_pair_kernel<BN><<<static_cast<unsigned>(2 * clusters), NUM_THREADS, PairCfg<BN>::SMEM_BYTES,
+                                         stream>>>(tmA, tmB, tmD, p);
     } else {
         int64_t grid = sms;
         if (a.offsets == nullptr) {
@@ -1189,10 +1060,7 @@ cudaError_t launch_fp8_block_gemm(const GemmArgs& a, cudaStream_t stream, int* l
     cudaError_t e = device_info(sms);
     if (e != cudaSuccess) return e;
     switch (choose_kind(a)) {
-        case 128: e = launch_cfg<128>(a, encode, sms, stream); break;
         case 256: e = launch_cfg<256>(a, encode, sms, stream); break;
-        case 1128: e = launch_cfg<1128>(a, encode, sms, stream); break;
-        case 2256: e = launch_cfg<2256>(a, encode, sms, stream); break;
         default: e = launch_cfg<1256>(a, encode, sms, stream); break;
     }
     if (e == cudaSuccess) *launches = 1;

@@ -328,11 +328,11 @@ print("kind ok")
 """
 
 
-@pytest.mark.parametrize("kind", ["128", "256", "1128", "2256"])
-def test_gemm_dev_kinds(kind):
-    # The dev tile kinds (FP8Q_GEMM_KIND; production picks 1256 / 256 / the decode kernel) stay
-    # correct and terminate -- kind 1128 once hung (its store warps waited for slices the
-    # 128-column promotion path never parks).  A fresh process per kind: the override is read once.
+@pytest.mark.parametrize("kind", ["256", "1256"])
+def test_gemm_forced_kinds(kind):
+    # Both tile kernels (FP8Q_GEMM_KIND forces one: 256 = one-CTA 128 x 256 tiles, 1256 = CTA pair
+    # 256 x 256) are correct on every shape, including the shapes production sends to the other
+    # one.  A fresh process per kind: the override is read once.
     import os
     import subprocess
     import sys
