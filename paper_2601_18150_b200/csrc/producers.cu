@@ -10,15 +10,21 @@
 // touches HBM unless the caller asks for it (optional y_out), saving 4 B per element of
 // traffic (2 written + 2 read).  The quantization of y is exactly quantize_act_per_token_group
 // applied to the BF16 y (same amax / scale / guarded-Markstein / satfinite element map).
-// The producer arithmetic is binary32: sum of squares per lane in element order, then a
-// xor-shuffle tree; inv = rsqrt_rn(mean + eps); y = RN(RN(x inv) gamma) -> BF16 RNE.
-// RMSNorm makes two passes over the row (the second hits L2), so HBM sees x once.
-// silu(g) = g * sigmoid(g) in an overflow-free form with approximate exp2 / reciprocal (see
-// silu2(): a few binary32 ulps).  All element math runs on binary32 PAIRS (FMUL2 / FFMA2 /
-// FADD2: one instruction for two correctly rounded operations, packed.cuh) -- these kernels
-// are instruction-bound, not HBM-bound, with scalar math.  (The oracle evaluates the producers in
-// binary64; the two BF16 results agree except for rare ties, see tests/test_gpu_producers.py.)
+//
+// Producer arithmetic = DESIGN.md reading N2 (Qwen3's HF modules: binary32, two BF16
+// roundings), bit-exact by construction:
+//   RMSNorm   ms = RN32(sum x^2 / K) with the sum EXACT: lanes accumulate the (exact) binary64
+//             squares; when the binary64 mean lies within its error bound of a binary32
+//             rounding boundary (~2^-14 of rows) the warp recomputes the sum exactly in a
+//             576-bit integer accumulator and rounds the exact quotient (exact_mean_sq);
+//             r = __frsqrt_rn(__fadd_rn(ms, eps)) (IEEE); t = RN_BF16(RN32(x r));
+//             y = RN_BF16(RN32(gamma t)).
+//   SiLU-mul  s = RN_BF16(silu(g)) depends only on the 16 bits of g: a 65,536-entry table built
+//             once per device by silu_table_kernel (binary64 exp, rounded directly to BF16;
+//             the exhaustive GPU test checks every entry against the oracle's 60-digit value),
+//             staged in shared memory; y = RN_BF16(RN32(s u)).
 #include <cstdint>
+#include <mutex>
 
 #include "packed.cuh"
 #include "ptx.cuh"
@@ -92,32 +98,6 @@ __device__ __forceinline__ uint2 quantize8(const uint4& y, uint32_t ab, int lane
     }
     return fast ? encode8_fast(y, s, r) : encode8_slow(y, s);
 }
-// silu(g) = g * sigmoid(g) without overflow: with e = exp(-|g|) (never overflows),
-// sigmoid = 1 / (1 + e) for g >= 0 and e / (1 + e) for g < 0.  exp via ex2.approx (no ftz:
-// subnormal e stay exact enough for BF16 subnormal outputs) and rcp.approx: a few binary32
-// ulps, far below the 2^-8 relative spacing of the BF16 result.
-__device__ __forceinline__ float ex2_approx(float x) {
-    float r;
-    asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ uint64_t silu2(uint64_t g2) {
-    const uint64_t a2 = g2 & 0x7FFFFFFF7FFFFFFFull;  // |g|
-    const uint64_t t2 = mul2(a2, pack2(-1.4426950408889634f, -1.4426950408889634f));
-    const float e0 = ex2_approx(lo_of(t2)), e1 = ex2_approx(hi_of(t2));
-    const uint64_t d2 = add2(pack2(e0, e1), pack2(1.0f, 1.0f));
-    const float r0 = rcp_approx(lo_of(d2)), r1 = rcp_approx(hi_of(d2));
-    const uint64_t er2 = mul2(pack2(e0, e1), pack2(r0, r1));
-    // sigmoid: r for g >= 0, e r for g < 0 (selected by the sign bit of g)
-    const float sg0 = (lo_of(g2) >= 0.0f) ? r0 : lo_of(er2);
-    const float sg1 = (hi_of(g2) >= 0.0f) ? r1 : hi_of(er2);
-    return mul2(g2, pack2(sg0, sg1));
-}
 __device__ __forceinline__ uint4 ld_nc(const void* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -127,57 +107,161 @@ __device__ __forceinline__ uint4 ld_nc(const void* p) {
 }
 
 // ---------------------------------------------------------------------------------------
+// RMSNorm mean of squares, exactly rounded: ms = RN32(S / K), S = sum x^2 over the BF16 row.
+//
+// Fast path: every lane holds the binary64 sum of its squares (each square is exact in
+// binary64: 16 significant bits), the warp reduces them (xor butterfly, so all lanes hold the
+// same s); relative error <= (terms per lane + 6) u64.  RN32(s / K) is then the correct
+// rounding unless s / K lies within that error of a binary32 rounding boundary (or outside the
+// binary32 normal range): there the warp takes exact_mean_sq.
+//
+// exact_mean_sq: S * 2^266 is an integer (x^2 = m^2 2^(2e), m <= 255, 2e >= -266) of < 534
+// bits: each lane adds its squares into an 18-word accumulator, the warp sums the accumulators
+// with carries, and the exact quotient S / K is rounded to nearest even by integer long
+// division (remainder = sticky bit).
+constexpr int kSqWords = 18;
+__device__ __forceinline__ void acc_add_sq(uint32_t (&acc)[kSqWords], uint32_t b) {
+    b &= 0x7FFFu;
+    if (b == 0u) return;
+    const uint32_t E = b >> 7;
+    const uint32_t m = E ? ((b & 0x7Fu) | 0x80u) : (b & 0x7Fu);
+    const uint32_t pos = E ? 2u * E - 2u : 0u;  // 2 e + 266 with e = E - 134 (E = 0: e = -133)
+    const uint64_t v = static_cast<uint64_t>(m * m) << (pos & 31u);
+    uint32_t w = pos >> 5;
+    uint64_t cur = static_cast<uint64_t>(acc[w]) + static_cast<uint32_t>(v);
+    acc[w] = static_cast<uint32_t>(cur);
+    cur = (cur >> 32) + acc[w + 1] + static_cast<uint32_t>(v >> 32);
+    acc[w + 1] = static_cast<uint32_t>(cur);
+    for (w += 2; (cur >> 32) != 0 && w < kSqWords; ++w) {
+        cur = static_cast<uint64_t>(acc[w]) + 1u;
+        acc[w] = static_cast<uint32_t>(cur);
+    }
+}
+__device__ __noinline__ float exact_mean_sq(const uint16_t* __restrict__ xrow, int k) {
+    const int lane = threadIdx.x & 31;
+    uint32_t acc[kSqWords];
+#pragma unroll
+    for (int i = 0; i < kSqWords; ++i) acc[i] = 0u;
+    for (int j = lane; j < k; j += 32) acc_add_sq(acc, xrow[j]);
+    for (int off = 16; off >= 1; off >>= 1) {  // butterfly: every lane ends with the total
+        uint64_t carry = 0;
+#pragma unroll
+        for (int i = 0; i < kSqWords; ++i) {
+            const uint64_t cur = carry + acc[i] + __shfl_xor_sync(0xFFFFFFFFu, acc[i], off);
+            acc[i] = static_cast<uint32_t>(cur);
+            carry = cur >> 32;
+        }
+    }
+    // N = S 2^266 2^64 (two zero words below: the quotient keeps >= 51 bits for any S > 0)
+    constexpr int NW = kSqWords + 2;
+    uint32_t q[NW];
+    uint64_t rem = 0;
+    const uint32_t kk = static_cast<uint32_t>(k);
+    for (int i = NW - 1; i >= 0; --i) {
+        const uint64_t cur = (rem << 32) | (i >= 2 ? acc[i - 2] : 0u);
+        q[i] = static_cast<uint32_t>(cur / kk);
+        rem = cur - static_cast<uint64_t>(q[i]) * kk;
+    }
+    int top = -1;  // most significant set bit of the quotient
+    for (int i = NW - 1; i >= 0 && top < 0; --i)
+        if (q[i] != 0u) top = 32 * i + 31 - __clz(q[i]);
+    if (top < 0) return 0.0f;  // S == 0
+    // value = (Q + rem / K) 2^e0; keep 24 bits (or fewer: binary32 subnormal quantum 2^-149)
+    constexpr int e0 = -266 - 64;
+    const int lsb = max(top - 23, -149 - e0);
+    auto bit = [&](int p) -> uint32_t { return p < 0 ? 0u : (q[p >> 5] >> (p & 31)) & 1u; };
+    uint32_t kept = 0;
+    for (int p = lsb + 23; p >= lsb; --p) kept = (kept << 1) | bit(p);
+    bool sticky = rem != 0;
+    for (int p = lsb - 2; p >= 0 && !sticky; --p) sticky = bit(p) != 0u;
+    if (bit(lsb - 1) && (sticky || (kept & 1u))) ++kept;
+    int ex = lsb + e0;  // value = kept 2^ex
+    if (kept == (1u << 24)) {
+        kept >>= 1;
+        ++ex;
+    }
+    if (kept < (1u << 23)) return __uint_as_float(kept);  // subnormal (ex == -149)
+    const int E = ex + 150;
+    if (E >= 255) return __uint_as_float(0x7F800000u);
+    return __uint_as_float((static_cast<uint32_t>(E) << 23) | (kept - (1u << 23)));
+}
+// s: the warp's binary64 sum of squares (identical in every lane); terms: squares per lane.
+__device__ __forceinline__ float mean_sq_rn(double s, int k, int terms, const uint16_t* __restrict__ xrow) {
+    if (!(s < 1.0e300)) return static_cast<float>(s);  // non-finite input: flagged downstream
+    const double q = __ddiv_rn(s, static_cast<double>(k));
+    if (q == 0.0) return 0.0f;
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(q));
+    const int E64 = static_cast<int>((b >> 52) & 0x7FF);
+    bool amb = true;
+    if (E64 >= 1023 - 126 && E64 <= 1023 + 126) {  // binary32 normal, away from overflow
+        const int64_t L = static_cast<int64_t>(b & ((1ull << 29) - 1));
+        const int64_t d = L - (1ll << 28);  // distance to the binary32 midpoint, in ulp64
+        amb = (d < 0 ? -d : d) <= 2 * (terms + 8);
+    }
+    if (!amb) return __double2float_rn(q);
+    return exact_mean_sq(xrow, k);
+}
+
 // RMSNorm + quantize: one warp per token row (persistent over rows).  Pass 1 streams the row
-// (HBM) and accumulates the sum of squares; pass 2 re-reads it (L2 hit: the row was read a
-// moment ago), normalises, rounds to BF16 and quantizes.  Vector t of lane l covers channels
-// 256 t + 8 l .. +7, i.e. group 2t + (l >= 16).  Few registers -> many warps per SM, and
-// UNROLL independent 16-byte loads per lane in flight in pass 1.
+// (HBM) and accumulates the binary64 sum of squares; pass 2 re-reads it (L2 hit: the row was
+// read a moment ago), normalises, rounds to BF16 and quantizes.  Vector t of lane l covers
+// channels 256 t + 8 l .. +7, i.e. group 2t + (l >= 16).  NV > 0: k = 256 NV (every Qwen3
+// hidden size), compile-time trip counts; NV == 0: any k % 128 == 0 (lane predicates).
+// (Measured alternative: keeping the row in registers between the passes instead of
+// re-reading it from L2 halves the occupancy and is 20 % slower.)
+template <int NV>
 __global__ void __launch_bounds__(256, 3) rmsnorm_quantize_kernel(
-    const uint16_t* __restrict__ x, const uint16_t* __restrict__ gamma, float eps, int64_t m, int64_t k,
+    const uint16_t* __restrict__ x, const uint16_t* __restrict__ gamma, float eps, int64_t m, int64_t k_rt,
     int64_t ld_x, uint8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scales, int64_t ld_s,
     uint16_t* __restrict__ y_out, int64_t ld_y, int32_t* __restrict__ flag) {
-    constexpr int UNROLL = 8;
+    const int k = NV > 0 ? NV * 256 : static_cast<int>(k_rt);
+    const int T = NV > 0 ? NV : (k + 255) / 256;
+    constexpr int P1 = NV > 0 && NV < 8 ? NV : 8;  // pass-1 loads in flight per lane
+    constexpr int U2 = NV > 0 && NV < 4 ? NV : 4;  // pass-2 vectors (x and gamma) loaded before use
     __shared__ ScaleTables tabs;
     init_scale_tables(tabs);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
-    const int T = static_cast<int>((k + 255) / 256);
     for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); row < m; row += warps) {
-        const uint16_t* xr = x + row * ld_x + lane * 8;
-        // pass 1: sum of squares, two interleaved binary32 partial sums per lane (FFMA2)
-        uint64_t ss2 = 0;
-        for (int t0 = 0; t0 < T; t0 += UNROLL) {
-            uint4 v[UNROLL];
+        const uint16_t* xrow = x + row * ld_x;
+        const uint16_t* xr = xrow + lane * 8;
+        // pass 1: binary64 sum of squares (two accumulators per lane)
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll 1
+        for (int t0 = 0; t0 < T; t0 += P1) {
+            uint4 v[P1];
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
+            for (int u = 0; u < P1; ++u) {
                 v[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (t0 + u < T && (t0 + u) * 256 + lane * 8 < k) v[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
+                if ((NV > 0 && NV % P1 == 0) || (t0 + u < T && (t0 + u) * 256 + lane * 8 < k))
+                    v[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
             }
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
+            for (int u = 0; u < P1; ++u) {
                 const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const uint64_t x2 = bf16x2_to_f32x2(w[i]);
-                    ss2 = fma2(x2, x2, ss2);
+                    const double lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
+                    s0 = fma(lo, lo, s0);
+                    s1 = fma(hi, hi, s1);
                 }
             }
         }
-        float ss = __fadd_rn(lo_of(ss2), hi_of(ss2));
+        double s = s0 + s1;
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xFFFFFFFFu, ss, off);
-        const float mean = __fdiv_rn(ss, static_cast<float>(k));
-        const float inv = __frsqrt_rn(__fadd_rn(mean, eps));
-        const uint64_t inv2 = pack2(inv, inv);
-        constexpr int U2 = 4;  // pass 2: U2 vectors of x and gamma loaded before any use
+        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
+        const float ms = mean_sq_rn(s, k, 8 * T, xrow);
+        const float r = __frsqrt_rn(__fadd_rn(ms, eps));
+        const uint64_t r2 = pack2(r, r);
+#pragma unroll 1
         for (int t0 = 0; t0 < T; t0 += U2) {
             uint4 xv[U2], gv[U2];
 #pragma unroll
             for (int u = 0; u < U2; ++u) {
                 const int col = (t0 + u) * 256 + lane * 8;
                 xv[u] = gv[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (t0 + u < T && col < k) {
+                if ((NV > 0 && NV % U2 == 0) || (t0 + u < T && col < k)) {
                     xv[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
                     gv[u] = __ldg(reinterpret_cast<const uint4*>(gamma + col));
                 }
@@ -192,8 +276,10 @@ __global__ void __launch_bounds__(256, 3) rmsnorm_quantize_kernel(
                 const uint32_t gw[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
                 uint32_t o[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i)  // y = RN(RN(x inv) gamma), rounded to BF16
-                    o[i] = f32x2_to_bf16x2(mul2(mul2(bf16x2_to_f32x2(w[i]), inv2), bf16x2_to_f32x2(gw[i])));
+                for (int i = 0; i < 4; ++i) {  // t = RN_BF16(RN32(x r)); y = RN_BF16(RN32(gamma t))
+                    const uint32_t tb = f32x2_to_bf16x2(mul2(bf16x2_to_f32x2(w[i]), r2));
+                    o[i] = f32x2_to_bf16x2(mul2(bf16x2_to_f32x2(tb), bf16x2_to_f32x2(gw[i])));
+                }
                 const uint4 y = make_uint4(o[0], o[1], o[2], o[3]);  // zeros past k (x and gamma were 0)
                 if (y_out != nullptr && col < k) st_v4(y_out + row * ld_y + col, y.x, y.y, y.z, y.w);
                 // the whole warp reduces (lanes of a dead half contribute zeros and store nothing)
@@ -208,120 +294,115 @@ __global__ void __launch_bounds__(256, 3) rmsnorm_quantize_kernel(
     }
 }
 
-// The same computation for k = 256 NV (every Qwen3 hidden size): all loops have compile-time
-// trip counts and no lane predicates (no divergence bookkeeping around the shuffles).
-// (Measured alternative: keeping the row in registers between the passes instead of
-// re-reading it from L2 halves the occupancy and is 20 % slower.)
-template <int NV>
-__global__ void __launch_bounds__(256, 3) rmsnorm_quantize_fixed_kernel(
-    const uint16_t* __restrict__ x, const uint16_t* __restrict__ gamma, float eps, int64_t m, int64_t ld_x,
-    uint8_t* __restrict__ q, int64_t ld_q, float* __restrict__ scales, int64_t ld_s, uint16_t* __restrict__ y_out,
-    int64_t ld_y, int32_t* __restrict__ flag) {
-    constexpr int K = NV * 256;
-    constexpr int P1 = NV < 8 ? NV : 8;  // pass-1 loads in flight per lane
-    constexpr int U2 = NV < 4 ? NV : 4;  // pass-2 vectors (x and gamma) loaded before use
-    __shared__ ScaleTables tabs;
-    init_scale_tables(tabs);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
-    const uint16_t* gl = gamma + lane * 8;
-    for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); row < m; row += warps) {
-        const uint16_t* xr = x + row * ld_x + lane * 8;
-        uint8_t* qr = q + row * ld_q + lane * 8;
-        uint64_t ss2 = 0;
-#pragma unroll 1
-        for (int t0 = 0; t0 < NV; t0 += P1) {
-            uint4 v[P1];
-#pragma unroll
-            for (int u = 0; u < P1; ++u) v[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
-#pragma unroll
-            for (int u = 0; u < P1; ++u) {
-                const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint64_t x2 = bf16x2_to_f32x2(w[i]);
-                    ss2 = fma2(x2, x2, ss2);
-                }
+// ---------------------------------------------------------------------------------------
+// SiLU table: g_silu_tab[b] = RN_BF16(silu(g)) for the BF16 bit pattern b of g (NaN for
+// non-finite g).  Built once per device (binary64: exp <= 1 ulp, one division, then a direct
+// binary64 -> BF16 rounding; tests/test_gpu_producers.py checks all 65,536 entries against the
+// oracle's correctly rounded values).
+__device__ uint16_t g_silu_tab[1 << 16];
+
+// binary64 -> BF16 bits, round to nearest even, one rounding.
+__device__ __forceinline__ uint32_t f64_to_bf16_rn(double v) {
+    const uint64_t u = static_cast<uint64_t>(__double_as_longlong(v));
+    const uint32_t sign = static_cast<uint32_t>(u >> 48) & 0x8000u;
+    const double a = fabs(v);
+    if (a < 1.1754943508222875e-38) {  // BF16 subnormal range: quantum 2^-133 (a 2^133 is exact)
+        return sign | static_cast<uint32_t>(rint(a * 1.0889035741470030e40));
+    }
+    const uint64_t mag = u & 0x7FFFFFFFFFFFFFFFull;
+    const uint64_t r = (mag + 0xFFFFFFFFFFFull + ((mag >> 45) & 1u)) >> 45;  // [E64 | 7 fraction bits]
+    const uint64_t bits = r - (896ull << 7);                                  // rebias 1023 -> 127
+    return sign | static_cast<uint32_t>(bits >= 0x7F80u ? 0x7F80u : bits);
+}
+__global__ void __launch_bounds__(256) silu_table_kernel() {
+    const uint32_t b = blockIdx.x * 256u + threadIdx.x;
+    uint32_t out;
+    if (((b >> 7) & 0xFFu) == 0xFFu) {
+        out = 0x7FC0u;
+    } else {
+        const double g = __uint_as_float(b << 16);
+        if (g == 0.0 || g > 200.0) {
+            out = b;  // silu(+-0) = +-0; g > 200: g (1 - e^-g) with e^-g < 1e-86 rounds to g
+        } else if (g < -200.0) {
+            out = 0x8000u;  // |silu| < 200 e^-200, below half the smallest BF16 subnormal
+        } else if (fabs(g) < 0x1p-30) {
+            // silu(g) = g/2 + g^2/4 + O(g^4): relative to g/2 the perturbation is below 2^-31,
+            // invisible to binary64 but it decides exact BF16 ties.  g/2 is exact; below 2^-126
+            // (BF16 subnormal quantum 2^-133) it can be an odd multiple of 2^-134, a tie that
+            // the positive g^2/4 breaks towards +infinity.
+            const double h = 0.5 * g;
+            const double t = fabs(h) * 0x1p133;  // exact
+            if (fabs(h) < 0x1p-126 && t - floor(t) == 0.5) {
+                const uint32_t mag = static_cast<uint32_t>(g > 0.0 ? ceil(t) : floor(t));
+                out = (g < 0.0 ? 0x8000u : 0u) | mag;
+            } else {
+                out = f64_to_bf16_rn(h);
             }
-        }
-        float ss = __fadd_rn(lo_of(ss2), hi_of(ss2));
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xFFFFFFFFu, ss, off);
-        const float inv = __frsqrt_rn(__fadd_rn(__fdiv_rn(ss, static_cast<float>(K)), eps));
-        const uint64_t inv2 = pack2(inv, inv);
-#pragma unroll 1
-        for (int t0 = 0; t0 < NV; t0 += U2) {
-            uint4 xv[U2], gv[U2];
-#pragma unroll
-            for (int u = 0; u < U2; ++u) {
-                xv[u] = *reinterpret_cast<const uint4*>(xr + (t0 + u) * 256);
-                gv[u] = __ldg(reinterpret_cast<const uint4*>(gl + (t0 + u) * 256));
-            }
-#pragma unroll
-            for (int u = 0; u < U2; ++u) {
-                const int t = t0 + u;
-                const uint32_t w[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
-                const uint32_t gw[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
-                uint32_t o[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)  // y = RN(RN(x inv) gamma), rounded to BF16
-                    o[i] = f32x2_to_bf16x2(mul2(mul2(bf16x2_to_f32x2(w[i]), inv2), bf16x2_to_f32x2(gw[i])));
-                const uint4 y = make_uint4(o[0], o[1], o[2], o[3]);
-                if (y_out != nullptr) st_v4(y_out + row * ld_y + t * 256 + lane * 8, y.x, y.y, y.z, y.w);
-                const uint32_t ab = group_amax(absmax_bits8(y));
-                const int g = t * 2 + (lane >> 4);
-                const uint2 c = quantize8(y, ab, lane, scales + g * ld_s + row, flag, tabs);
-                st_stream_v2(qr + t * 256, c.x, c.y);
-            }
+        } else {
+            out = f64_to_bf16_rn(g / (1.0 + exp(-g)));
         }
     }
+    g_silu_tab[b] = static_cast<uint16_t>(out);
 }
 
-// ---------------------------------------------------------------------------------------
-// SiLU(gate) * up + quantize: one warp per (token row, chunk of 8 output groups); vector j of
+// SiLU(gate) * up + quantize: persistent CTAs of 16 warps; the table is staged into shared
+// memory (128 KB) once per CTA; a warp item = (token row, chunk of 8 output groups); vector j of
 // lane l covers outputs chunk*1024 + 256 j + 8 l .. +7 (group 2j + (l >= 16)).
+constexpr int SILU_THREADS = 512;
+constexpr size_t SILU_SMEM = (size_t(1) << 17);
 template <bool FULL>
-__global__ void __launch_bounds__(256) silu_mul_quantize_kernel(
+__global__ void __launch_bounds__(SILU_THREADS, 1) silu_mul_quantize_kernel(
     const uint16_t* __restrict__ gu, int64_t m, int64_t inter, int64_t ld_gu, uint8_t* __restrict__ q,
     int64_t ld_q, float* __restrict__ scales, int64_t ld_s, uint16_t* __restrict__ y_out, int64_t ld_y,
     int64_t chunks, int32_t* __restrict__ flag) {
+    extern __shared__ __align__(16) uint16_t stab[];
     __shared__ ScaleTables tabs;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(g_silu_tab);
+        uint4* dst = reinterpret_cast<uint4*>(stab);
+        for (int i = threadIdx.x; i < (1 << 16) / 8; i += SILU_THREADS) dst[i] = src[i];
+    }
     init_scale_tables(tabs);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (item >= m * chunks) return;
-    const int64_t row = item / chunks;
-    const int chunk = static_cast<int>(item - row * chunks);
     const int groups = static_cast<int>(inter >> 7);
-    const uint16_t* gr = gu + row * ld_gu + (lane & 15) * 8;
-    uint4 gv[4], uv[4];
+    const int64_t items = m * chunks;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (SILU_THREADS / 32);
+    for (int64_t item = static_cast<int64_t>(blockIdx.x) * (SILU_THREADS / 32) + (threadIdx.x >> 5); item < items;
+         item += nwarps) {
+        const int64_t row = item / chunks;
+        const int chunk = static_cast<int>(item - row * chunks);
+        const uint16_t* gr = gu + row * ld_gu + (lane & 15) * 8;
+        uint4 gv[4], uv[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int g = chunk * 8 + 2 * j + (lane >> 4);
-        gv[j] = uv[j] = make_uint4(0u, 0u, 0u, 0u);
-        if (FULL || g < groups) {
-            gv[j] = ld_nc(gr + g * 128);
-            uv[j] = ld_nc(gr + inter + g * 128);
+        for (int j = 0; j < 4; ++j) {
+            const int g = chunk * 8 + 2 * j + (lane >> 4);
+            gv[j] = uv[j] = make_uint4(0u, 0u, 0u, 0u);
+            if (FULL || g < groups) {
+                gv[j] = ld_nc(gr + g * 128);
+                uv[j] = ld_nc(gr + inter + g * 128);
+            }
         }
-    }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int g = chunk * 8 + 2 * j + (lane >> 4);
-        const uint32_t gw[4] = {gv[j].x, gv[j].y, gv[j].z, gv[j].w};
-        const uint32_t uw[4] = {uv[j].x, uv[j].y, uv[j].z, uv[j].w};
-        uint32_t o[4];
+        for (int j = 0; j < 4; ++j) {
+            const int g = chunk * 8 + 2 * j + (lane >> 4);
+            const uint32_t gw[4] = {gv[j].x, gv[j].y, gv[j].z, gv[j].w};
+            const uint32_t uw[4] = {uv[j].x, uv[j].y, uv[j].z, uv[j].w};
+            uint32_t o[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)  // y = RN(silu(g) u), rounded to BF16
-            o[i] = f32x2_to_bf16x2(mul2(silu2(bf16x2_to_f32x2(gw[i])), bf16x2_to_f32x2(uw[i])));
-        const uint4 y = make_uint4(o[0], o[1], o[2], o[3]);
-        const uint32_t ab = group_amax(absmax_bits8(y));
-        if (FULL || g < groups) {
-            const int col = g * 128 + (lane & 15) * 8;
-            if (y_out != nullptr) st_v4(y_out + row * ld_y + col, y.x, y.y, y.z, y.w);
-            const uint2 c = quantize8(y, ab, lane, scales + int64_t(g) * ld_s + row, flag, tabs);
-            st_stream_v2(q + row * ld_q + col, c.x, c.y);
+            for (int i = 0; i < 4; ++i) {  // y = RN_BF16(RN32(s u)), s = table[g]
+                const uint32_t sb = static_cast<uint32_t>(stab[gw[i] & 0xFFFFu]) |
+                                    (static_cast<uint32_t>(stab[gw[i] >> 16]) << 16);
+                o[i] = f32x2_to_bf16x2(mul2(bf16x2_to_f32x2(sb), bf16x2_to_f32x2(uw[i])));
+            }
+            const uint4 y = make_uint4(o[0], o[1], o[2], o[3]);
+            const uint32_t ab = group_amax(absmax_bits8(y));
+            if (FULL || g < groups) {
+                const int col = g * 128 + (lane & 15) * 8;
+                if (y_out != nullptr) st_v4(y_out + row * ld_y + col, y.x, y.y, y.z, y.w);
+                const uint2 c = quantize8(y, ab, lane, scales + int64_t(g) * ld_s + row, flag, tabs);
+                st_stream_v2(q + row * ld_q + col, c.x, c.y);
+            }
         }
     }
 }
@@ -346,35 +427,97 @@ cudaError_t launch_rmsnorm_quantize(const uint16_t* x, const uint16_t* gamma, fl
     const unsigned grid = static_cast<unsigned>(rows_blocks < cap ? rows_blocks : cap);
     if (k % 256 == 0 && k <= 4096) {
         switch (k / 256) {
-#define RMS_FIXED(NV)                                                                                      \
-    case NV:                                                                                               \
-        rmsnorm_quantize_fixed_kernel<NV><<<grid, 256, 0, stream>>>(x, gamma, eps, m, ld_x, q, ld_q, scales, \
-                                                                    ld_s, y, ld_y, flag);                  \
+#define RMS_FIXED(NV)                                                                                        \
+    case NV:                                                                                                 \
+        rmsnorm_quantize_kernel<NV><<<grid, 256, 0, stream>>>(x, gamma, eps, m, k, ld_x, q, ld_q, scales, ld_s, \
+                                                              y, ld_y, flag);                                 \
         return cudaGetLastError();
-            RMS_FIXED(1) RMS_FIXED(2) RMS_FIXED(3) RMS_FIXED(4) RMS_FIXED(5) RMS_FIXED(6) RMS_FIXED(7)
-            RMS_FIXED(8) RMS_FIXED(9) RMS_FIXED(10) RMS_FIXED(11) RMS_FIXED(12) RMS_FIXED(13) RMS_FIXED(14)
-            RMS_FIXED(15) RMS_FIXED(16)
+            RMS_FIXED(1) RMS_FIXED(2) RMS_FIXED(4) RMS_FIXED(8) RMS_FIXED(12) RMS_FIXED(16)
 #undef RMS_FIXED
             default: break;
         }
     }
-    rmsnorm_quantize_kernel<<<grid, 256, 0, stream>>>(x, gamma, eps, m, k, ld_x, q, ld_q, scales, ld_s, y, ld_y, flag);
+    rmsnorm_quantize_kernel<0><<<grid, 256, 0, stream>>>(x, gamma, eps, m, k, ld_x, q, ld_q, scales, ld_s, y, ld_y,
+                                                         flag);
     return cudaGetLastError();
 }
+
+namespace {
+// The SiLU table is built once per device, on the first launch's stream.  Later launches on
+// other streams wait for that build (cudaStreamWaitEvent) until it has been seen complete; a
+// launch inside a stream capture before then captures its own (idempotent) build.
+struct SiluTableState {
+    bool launched = false;
+    bool complete = false;
+    bool smem_attr = false;
+    cudaEvent_t built = nullptr;
+};
+SiluTableState g_silu_state[64];
+std::mutex g_silu_mu;
+
+cudaError_t ensure_silu_table(cudaStream_t stream) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_silu_mu);
+    SiluTableState& st = g_silu_state[dev];
+    if (!st.smem_attr) {
+        e = cudaFuncSetAttribute(silu_mul_quantize_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(SILU_SMEM));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(silu_mul_quantize_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(SILU_SMEM));
+        if (e != cudaSuccess) return e;
+        st.smem_attr = true;
+    }
+    if (st.complete) return cudaSuccess;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    e = cudaStreamIsCapturing(stream, &cap);
+    if (e != cudaSuccess) return e;
+    if (cap != cudaStreamCaptureStatusNone) {  // inside a capture: build as part of the graph
+        silu_table_kernel<<<256, 256, 0, stream>>>();
+        return cudaGetLastError();
+    }
+    if (!st.launched) {
+        silu_table_kernel<<<256, 256, 0, stream>>>();
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        if (st.built == nullptr) {
+            e = cudaEventCreateWithFlags(&st.built, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        e = cudaEventRecord(st.built, stream);
+        if (e != cudaSuccess) return e;
+        st.launched = true;
+        return cudaSuccess;
+    }
+    const cudaError_t qe = cudaEventQuery(st.built);
+    if (qe == cudaSuccess) {
+        st.complete = true;
+        return cudaSuccess;
+    }
+    if (qe != cudaErrorNotReady) return qe;
+    return cudaStreamWaitEvent(stream, st.built, 0);
+}
+}  // namespace
 
 cudaError_t launch_silu_mul_quantize(const uint16_t* gu, int64_t m, int64_t inter, int64_t ld_gu, uint8_t* q,
                                      int64_t ld_q, float* scales, int64_t ld_s, uint16_t* y, int64_t ld_y,
                                      int32_t* flag, cudaStream_t stream) {
     if (m == 0 || inter == 0) return cudaSuccess;
+    cudaError_t e = ensure_silu_table(stream);
+    if (e != cudaSuccess) return e;
     const int64_t chunks = (inter / 128 + 7) / 8;
     const int64_t items = m * chunks;
-    const int64_t blocks = (items + 7) / 8;
-    if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;
+    const int64_t per_cta = SILU_THREADS / 32;
+    int64_t grid = (items + per_cta - 1) / per_cta;
+    grid = grid < sms() ? grid : sms();
     if ((inter / 128) % 8 == 0)
-        silu_mul_quantize_kernel<true><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        silu_mul_quantize_kernel<true><<<static_cast<unsigned>(grid), SILU_THREADS, SILU_SMEM, stream>>>(
             gu, m, inter, ld_gu, q, ld_q, scales, ld_s, y, ld_y, chunks, flag);
     else
-        silu_mul_quantize_kernel<false><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        silu_mul_quantize_kernel<false><<<static_cast<unsigned>(grid), SILU_THREADS, SILU_SMEM, stream>>>(
             gu, m, inter, ld_gu, q, ld_q, scales, ld_s, y, ld_y, chunks, flag);
     return cudaGetLastError();
 }
