@@ -226,6 +226,29 @@ fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales
                            int64_t k, void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * fp8_linear_dynamic -- one W8A8 linear layer of the rollout forward as the engine calls it:
+ * the BF16 layer input quantized dynamically per token per 128 channels (the
+ * 1x128 granularity of PAPER.md:233) and multiplied by the blockwise-quantized weight
+ * (PAPER.md:99,129).  Result bit-identical to quantize_act_per_token_group(x) followed by
+ * fp8_block_gemm(codes, scales, b, b_scales) -- the same element map and the same GEMM.
+ *   x_bf16   [m, k] BF16 activations, row stride ld_x (16-byte aligned, ld_x % 8 == 0).
+ *   b, b_scales, d, d_dtype, m, n, k   as fp8_block_gemm.
+ *   nonfinite_flag  as quantize_act_per_token_group (set if x holds NaN/Inf; nullable).
+ *   workspace / workspace_bytes: at least fp8_linear_dynamic_workspace_size(m, n, k) bytes,
+ *     256-byte aligned, ZERO-FILLED before first use (the GEMM's split-K counters; every launch
+ *     leaves them zeroed).  Decode sizes (1 <= m <= 64 where the decode kernel applies) run ONE
+ *     kernel that quantizes the activations itself (no intermediate codes in HBM, no second
+ *     launch); their size may be 0, and NULL is then allowed.  Larger m run the two kernels,
+ *     the activation codes and scales living in the workspace (FP8Q_EWORKSPACE if missing).
+ *   Requirements as fp8_block_gemm (k % 128, n % 8, alignments).
+ */
+size_t fp8_linear_dynamic_workspace_size(int64_t m, int64_t n, int64_t k);
+fp8q_status fp8_linear_dynamic(const void* x_bf16, int64_t ld_x, const uint8_t* b, int64_t ld_b,
+                               const float* b_scales, int64_t ld_sb, void* d, int64_t ld_d, fp8q_out_dtype d_dtype,
+                               int64_t m, int64_t n, int64_t k, int32_t* nonfinite_flag, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+/*
  * fp8_block_gemm_grouped -- MoE expert layers in FP8 ("MoE expert layers
  * (fc1, fc2)").  Group g multiplies A rows [offsets[g], offsets[g+1]) by
  * B_g = b + g * stride_b (bytes) with scales b_scales + g * stride_sb (elements):
@@ -341,14 +364,6 @@ fp8q_status e4m3_encode_f32(const float* x, int64_t n, uint8_t* codes, void* str
  */
 int64_t fp8q_kernel_launches(void);
 
-/*
- * fp8q_debug_set_gemm_trace -- DEVELOPMENT ONLY.  When dev_ptr (device, >= 96*8 uint32) is
- * non-NULL, later fp8_block_gemm launches make CTA 0 write SM clock() stamps of its first 96
- * k-blocks' pipeline events (producer issue, MMA tmem-free / smem-full, promotion
- * partial-ready / release / done) to dev_ptr[kblock*12 + event].  NULL disables.  Not
- * thread-safe; never set in production.
- */
-void fp8q_debug_set_gemm_trace(uint32_t* dev_ptr);
 
 #ifdef __cplusplus
 }

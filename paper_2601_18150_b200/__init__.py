@@ -9,6 +9,7 @@ from .fp8q import (  # noqa: F401
     act_scales_ld,
     fp8_block_gemm,
     fp8_block_gemm_grouped,
+    fp8_linear_dynamic,
     fp8_mx_gemm,
     kernel_launches,
     mx_quantize,

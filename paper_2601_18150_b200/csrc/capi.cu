@@ -66,7 +66,6 @@ fp8q_status e4m3_encode_f32(const float* x, int64_t n, uint8_t* codes, void* str
     return from_cuda(e);
 }
 
-void fp8q_debug_set_gemm_trace(uint32_t* dev_ptr) { fp8q::set_gemm_trace(dev_ptr); }
 
 static fp8q_status check_weight(const void* w_bf16, int64_t n, int64_t k, int64_t ld_w, const uint8_t* codes,
                                 int64_t ld_q, const float* scales, int64_t ld_s) {
@@ -423,6 +422,94 @@ fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales
     g.workspace_bytes = workspace_bytes;
     int launched = 0;
     cudaError_t e = fp8q::launch_fp8_block_gemm(g, static_cast<cudaStream_t>(stream), &launched);
+    g_launches.fetch_add(launched);
+    return from_cuda(e);
+}
+
+// fp8_linear_dynamic: workspace = [GEMM split-K workspace][activation codes m x k][scales];
+// the fused decode kernel needs none of the last two.
+namespace {
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+int64_t act_ld_s(int64_t m) { return (m + 3) / 4 * 4; }
+fp8q::GemmArgs linear_args(const void* x_bf16, int64_t ld_x, const uint8_t* b, int64_t ld_b, const float* b_scales,
+                           int64_t ld_sb, void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
+                           int64_t k, int32_t* flag) {
+    fp8q::GemmArgs g{};
+    g.b = b;
+    g.ld_b = ld_b;
+    g.sb = b_scales;
+    g.ld_sb = ld_sb;
+    g.d = d;
+    g.ld_d = ld_d;
+    g.out_f32 = d_dtype == FP8Q_OUT_F32;
+    g.m = m;
+    g.n = n;
+    g.k = k;
+    g.groups = 1;
+    g.a_bf16 = static_cast<const uint16_t*>(x_bf16);
+    g.ld_a_bf16 = ld_x;
+    g.flag = flag;
+    return g;
+}
+}  // namespace
+
+size_t fp8_linear_dynamic_workspace_size(int64_t m, int64_t n, int64_t k) {
+    if (m <= 0 || n <= 0 || k <= 0) return 0;
+    fp8q::GemmArgs g = linear_args(reinterpret_cast<const void*>(16), k, nullptr, k, nullptr, k / 128, nullptr, n,
+                                   FP8Q_OUT_BF16, m, n, k, nullptr);
+    if (fp8q::skinny_gemm_applies(g)) return fp8q::skinny_workspace_bytes(m, n, k);  // fused: no act buffers
+    return align_up(fp8q::gemm_workspace_bytes(m, n, k, false)) + align_up(static_cast<size_t>(m * k)) +
+           static_cast<size_t>(k / 128) * act_ld_s(m) * 4;
+}
+
+fp8q_status fp8_linear_dynamic(const void* x_bf16, int64_t ld_x, const uint8_t* b, int64_t ld_b,
+                               const float* b_scales, int64_t ld_sb, void* d, int64_t ld_d, fp8q_out_dtype d_dtype,
+                               int64_t m, int64_t n, int64_t k, int32_t* nonfinite_flag, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+    if (workspace != nullptr && !aligned(workspace, 256)) return FP8Q_EALIGN;
+    if (m < 0 || n < 0 || k < 0 || ld_x < k) return FP8Q_EINVAL;
+    // the GEMM's checks with the activation codes' layout (ld = k) standing in for a
+    const uint8_t* fake_a = reinterpret_cast<const uint8_t*>(16);
+    fp8q_status st = gemm_common_checks(fake_a, (k + 15) / 16 * 16, reinterpret_cast<const float*>(16),
+                                        act_ld_s(m), b, ld_b, b_scales, ld_sb, d, ld_d, d_dtype, m, n, k);
+    if (st != FP8Q_OK || m == 0 || n == 0) return st;
+    if (x_bf16 == nullptr && k > 0) return FP8Q_EINVAL;
+    if (k > 0 && (!aligned(x_bf16, 16) || ld_x % 8 != 0)) return FP8Q_EALIGN;
+    if (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)) return FP8Q_EALIGN;
+    if (k == 0) return zero_output(d, ld_d, d_dtype, m, n, stream);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    fp8q::GemmArgs g = linear_args(x_bf16, ld_x, b, ld_b, b_scales, ld_sb, d, ld_d, d_dtype, m, n, k,
+                                   nonfinite_flag);
+    if (fp8q::skinny_gemm_applies(g)) {  // decode sizes: one launch, activations quantized in the GEMM
+        g.workspace = workspace;
+        g.workspace_bytes = workspace_bytes;
+        int launched = 0;
+        const cudaError_t e = fp8q::launch_fp8_block_gemm(g, s, &launched);
+        g_launches.fetch_add(launched);
+        return from_cuda(e);
+    }
+    // otherwise: quantize_act_per_token_group into the workspace, then fp8_block_gemm
+    const size_t gws = fp8q::gemm_workspace_bytes(m, n, k, false);
+    if (workspace == nullptr || workspace_bytes < fp8_linear_dynamic_workspace_size(m, n, k))
+        return FP8Q_EWORKSPACE;
+    char* base = static_cast<char*>(workspace);
+    uint8_t* codes = reinterpret_cast<uint8_t*>(base + align_up(gws));
+    float* scales = reinterpret_cast<float*>(base + align_up(gws) + align_up(static_cast<size_t>(m * k)));
+    cudaError_t e = fp8q::launch_act_per_token_group(static_cast<const uint16_t*>(x_bf16), m, k, ld_x, codes, k,
+                                                     scales, act_ld_s(m), nonfinite_flag, s);
+    if (e != cudaSuccess) return from_cuda(e);
+    g_launches.fetch_add(1);
+    g.a_bf16 = nullptr;
+    g.flag = nullptr;
+    g.a = codes;
+    g.ld_a = k;
+    g.sa = scales;
+    g.ld_sa = act_ld_s(m);
+    g.workspace = gws > 0 ? workspace : nullptr;
+    g.workspace_bytes = gws;
+    int launched = 0;
+    e = fp8q::launch_fp8_block_gemm(g, s, &launched);
     g_launches.fetch_add(launched);
     return from_cuda(e);
 }

@@ -845,7 +845,6 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-uint32_t* g_trace = nullptr;
 
 struct DeviceInfo {
     int sms = 0;
@@ -1032,9 +1031,7 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
 
 }  // namespace
 
-void set_gemm_trace(uint32_t* dev_ptr) { g_trace = dev_ptr; }
 void* tensor_map_encode_fn() { return reinterpret_cast<void*>(tensor_map_encoder()); }
-uint32_t* get_gemm_trace() { return g_trace; }
 
 size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped) {
     if (grouped || m <= 0 || n <= 0 || k <= 0) return 0;

@@ -1,0 +1,77 @@
+// group_quant.cuh -- the element map of the quantizers (readings Q1-Q7) as
+// device helpers shared by every kernel that writes E4M3 activations or weights: the
+// quantizers (quant.cu) and the decode GEMM's fused activation quantization
+// (gemm_skinny.cu), so all of them produce the same bytes by construction.
+//   amax bits: max over sign-cleared BF16 bit patterns (>= 0x7F80: non-finite input);
+//   s = RN32(amax / 448), amax == 0 -> 1 (division, or the table path of scale_tables.cuh);
+//   code = E4M3_RNE_satfinite(RN32(x / s)), guarded Markstein quotient for amax >= 2^-104,
+//   the sign of x re-imposed (-0 -> 0x80).
+#pragma once
+#include <cstdint>
+
+#include "packed.cuh"
+#include "ptx.cuh"
+
+namespace fp8q {
+
+constexpr uint32_t kAmaxFastGuardBits = 0x0B80u;  // BF16 bits of 2^-104
+constexpr uint32_t kNonFiniteBits = 0x7F80u;      // |x| bits >= this: Inf or NaN
+
+// max over the 8 sign-cleared BF16 bit patterns of a 16-byte vector
+__device__ __forceinline__ uint32_t vec_abs_max_bits(const uint4& v) {
+    const uint32_t m = 0x7FFF7FFFu;
+    uint32_t a = __vmaxu2(__vmaxu2(v.x & m, v.y & m), __vmaxu2(v.z & m, v.w & m));
+    return max(a & 0xFFFFu, a >> 16);
+}
+
+__device__ __forceinline__ float scale_from_amax_bits(uint32_t ab) {
+    // amax == 0 -> 1 (reading Q5); otherwise one IEEE binary32 division (reading Q4)
+    return ab == 0u ? 1.0f : __fdiv_rn(__uint_as_float(ab << 16), 448.0f);
+}
+
+// max(|a|, |b|) per BF16 lane in one HMNMX2 (.NaN: a NaN input gives the canonical NaN, so
+// NaN/Inf still surface as sign-cleared bits >= 0x7F80; the result's sign is garbage and is
+// masked once at the end).  For every non-NaN BF16 the float order of |x| is the integer order
+// of its sign-cleared bits, so this returns the same amax bits as the integer max it replaces
+// (3 ALU instructions per word pair -> 1).
+__device__ __forceinline__ uint32_t bmax_abs2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.NaN.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t abs_max_bits16(const uint32_t (&w)[8]) {
+    const uint32_t a = bmax_abs2(bmax_abs2(bmax_abs2(w[0], w[1]), bmax_abs2(w[2], w[3])),
+                                 bmax_abs2(bmax_abs2(w[4], w[5]), bmax_abs2(w[6], w[7]))) &
+                       0x7FFF7FFFu;
+    return max(a & 0xFFFFu, a >> 16);
+}
+// 16 BF16 (8 words) -> 16 E4M3 codes (4 words).
+template <bool kFast>
+__device__ __forceinline__ uint4 encode16(const uint32_t (&w)[8], float s, float r) {
+    const uint64_t rr = pack2(r, r);
+    const uint64_t nss = pack2(-s, -s);
+    uint32_t c[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
+        float q0, q1, q2, q3;
+        if (kFast) {
+            const uint64_t qa = quot2_fast(pack2(__uint_as_float(wa << 16), __uint_as_float(wa & 0xFFFF0000u)), rr, nss);
+            const uint64_t qb = quot2_fast(pack2(__uint_as_float(wb << 16), __uint_as_float(wb & 0xFFFF0000u)), rr, nss);
+            q0 = lo_of(qa);
+            q1 = hi_of(qa);
+            q2 = lo_of(qb);
+            q3 = hi_of(qb);
+        } else {
+            q0 = __fdiv_rn(__uint_as_float(wa << 16), s);
+            q1 = __fdiv_rn(__uint_as_float(wa & 0xFFFF0000u), s);
+            q2 = __fdiv_rn(__uint_as_float(wb << 16), s);
+            q3 = __fdiv_rn(__uint_as_float(wb & 0xFFFF0000u), s);
+        }
+        const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;  // input sign bits
+        c[i] = (cvt_e4m3x2(q0, q1) | (cvt_e4m3x2(q2, q3) << 16)) | sign;
+    }
+    return make_uint4(c[0], c[1], c[2], c[3]);
+}
+
+}  // namespace fp8q

@@ -68,7 +68,13 @@ struct GemmArgs {
     int32_t groups;
     void* workspace;         // split-K workspace (zero-filled before first use), may be null
     size_t workspace_bytes;
+    // fused activation quantization (decode kernel, m <= kSkinnyMaxXQ): BF16 activations
+    // instead of a / sa; the kernel quantizes them per token per 128 channels itself
+    const uint16_t* a_bf16 = nullptr;
+    int64_t ld_a_bf16 = 0;
+    int32_t* flag = nullptr;  // non-finite activation flag of the fused quantization
 };
+constexpr int kSkinnyMaxXQ = 64;
 
 // Decode-sized dense GEMMs (1 <= m <= kSkinnyMaxM) run the swap-AB kernel of gemm_skinny.cu
 // (m > 128 only where its cluster split-K mode applies).
@@ -108,8 +114,5 @@ cudaError_t launch_fp8_mx_gemm(const uint8_t* a, int64_t ld_a, const uint8_t* sf
                                int64_t k, void* encode_fn, cudaStream_t stream);
 void* tensor_map_encode_fn();
 
-// Dev-only: record a pipeline timeline of CTA 0 into dev_ptr (96 k-blocks x 12 uint32 clocks).
-void set_gemm_trace(uint32_t* dev_ptr);
-uint32_t* get_gemm_trace();
 
 }  // namespace fp8q

@@ -81,6 +81,11 @@ def load_library() -> ctypes.CDLL:
         lib.fp8_block_gemm.argtypes = [P, I64, P, I64, P, I64, P, I64, P, I64, ctypes.c_int,
                                        I64, I64, I64, P, ctypes.c_size_t, P]
         lib.fp8_block_gemm.restype = ctypes.c_int
+        lib.fp8_linear_dynamic_workspace_size.argtypes = [I64, I64, I64]
+        lib.fp8_linear_dynamic_workspace_size.restype = ctypes.c_size_t
+        lib.fp8_linear_dynamic.argtypes = [P, I64, P, I64, P, I64, P, I64, ctypes.c_int, I64, I64, I64, P, P,
+                                           ctypes.c_size_t, P]
+        lib.fp8_linear_dynamic.restype = ctypes.c_int
         lib.fp8_block_gemm_grouped_workspace_size.argtypes = [I64, I64, I64, I32]
         lib.fp8_block_gemm_grouped_workspace_size.restype = ctypes.c_size_t
         lib.fp8_block_gemm_grouped.argtypes = [P, I64, P, I64, P, I64, I64, P, I64, I64, P, I64,
@@ -408,6 +413,31 @@ def fp8_block_gemm(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_s
         a.data_ptr(), _ld(a), a_scales.data_ptr(), ld_sa, b.data_ptr(), _ld(b), b_scales.data_ptr(),
         ld_sb, out.data_ptr(), _ld(out), FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16,
         m, n, k, ws_ptr, ws_bytes, sh), "fp8_block_gemm")
+    return out
+
+
+def fp8_linear_dynamic(x: torch.Tensor, b: torch.Tensor, b_scales: torch.Tensor,
+                       out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None,
+                       nonfinite_flag: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """One W8A8 linear with dynamic activation quantization: BF16 x [m,k],
+    b codes [n,k], b_scales [ceil(n/128), >=k/128] -> D [m, n]; bit-identical to
+    quantize_act_per_token_group followed by fp8_block_gemm (decode sizes: one fused kernel)."""
+    _cuda2d(x, "x", torch.bfloat16)
+    _cuda2d(b, "b", torch.uint8)
+    _cuda2d(b_scales, "b_scales", torch.float32)
+    m, k = x.shape
+    n, kb = b.shape
+    if kb != k:
+        raise Fp8qError("fp8_linear_dynamic: inner dimensions differ")
+    out = _out(out, m, n, out_dtype, x.device)
+    ld_sb = _check_weight_scales(b_scales, n, k, "b_scales")
+    lib = load_library()
+    ws_ptr, ws_bytes = _workspace(x.device, stream, int(lib.fp8_linear_dynamic_workspace_size(m, n, k)))
+    flag = nonfinite_flag.data_ptr() if nonfinite_flag is not None else None
+    _check(lib.fp8_linear_dynamic(
+        x.data_ptr(), _ld(x), b.data_ptr(), _ld(b), b_scales.data_ptr(), ld_sb, out.data_ptr(), _ld(out),
+        FP8Q_OUT_F32 if out_dtype == torch.float32 else FP8Q_OUT_BF16, m, n, k, flag, ws_ptr, ws_bytes,
+        _stream(stream)), "fp8_linear_dynamic")
     return out
 
 

@@ -35,7 +35,7 @@ def test_header_declares_the_boundary():
                      "fp8q_kernel_launches", "rmsnorm_quantize_act_per_token_group",
                      "silu_mul_quantize_act_per_token_group", "kv_amax_update", "kv_scale_from_amax",
                      "kv_quantize_append", "quantize_weight_blockwise_fanout", "mx_scale_bytes", "mx_quantize",
-                     "fp8_mx_gemm", "quantize_act_per_token_group_batched", "quantize_weight_blockwise_batched"]:
+                     "fp8_mx_gemm", "quantize_act_per_token_group_batched", "quantize_weight_blockwise_batched", "fp8_linear_dynamic", "fp8_linear_dynamic_workspace_size"]:
         assert required in names
 
 
