@@ -372,15 +372,14 @@ def bench_decode(st: LayerStep, peaks, clocks, ms=(1, 64, 128, 256), copies=4, r
     t_win = time.perf_counter()
     for m in ms:
         xs = {nm: st.x[nm][:m] for nm, _, _ in LAYER}
-        xq = {nm: torch.empty((m, k), dtype=torch.uint8, device=dev) for nm, _, k in LAYER}
-        xsc = {nm: torch.empty((k // 128, fq.act_scales_ld(m)), dtype=torch.float32, device=dev) for nm, _, k in LAYER}
         ys = {nm: torch.empty((m, n), dtype=torch.bfloat16, device=dev) for nm, n, _ in LAYER}
 
         def layer(c, s, which=None):
+            # each linear as the rollout engine calls it: BF16 input, dynamic activation
+            # quantization + blockwise FP8 GEMM (one fused kernel at M <= 8, two launches above)
             for nm, _, _ in LAYER:
                 if which is None or nm == which:
-                    fq.quantize_act_per_token_group(xs[nm], xq[nm], xsc[nm])
-                    fq.fp8_block_gemm(xq[nm], xsc[nm], c[nm], s[nm], out=ys[nm])
+                    fq.fp8_linear_dynamic(xs[nm], c[nm], s[nm], out=ys[nm])
 
         def graph_us(which=None):
             s = torch.cuda.Stream(dev)
@@ -422,10 +421,12 @@ def bench_decode(st: LayerStep, peaks, clocks, ms=(1, 64, 128, 256), copies=4, r
                         "gemm_hbm_floor_us": round(gemm_floor_us, 2),
                         "layer_tflops": round(layer_flops(m) / (t_layer * 1e-6) / 1e12, 2)}
     del layers
-    return {"config": "BASELINE.json configs[2]: Qwen3-8B decode-shaped GEMMs (M tokens, real N, K), bf16 out",
+    return {"config": "BASELINE.json configs[2]: Qwen3-8B decode-shaped GEMMs (M tokens, real N, K), bf16 out; "
+                      "each linear = fp8_linear_dynamic (BF16 input quantized per token per 128 channels + "
+                      "blockwise FP8 GEMM: one fused kernel at M <= 8, two launches above)",
             "timing": f"one CUDA graph of {copies} layers x 4 replays (weights rotate over {copies} copies, "
-                      f"{copies} x 193 MB > L2), median of {replays} replays; per_gemm = graphs of one GEMM "
-                      "(+ its activation quantization) alone",
+                      f"{copies} x 193 MB > L2), median of {replays} replays; per_gemm = graphs of one linear "
+                      "(incl. its activation quantization) alone",
             "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peaks["hbm_gbs"],
                          "achieved_by_m": {k: v["GBps"] for k, v in out.items()},
                          "frac_by_m": {k: v["frac_hbm"] for k, v in out.items()}},

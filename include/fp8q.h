@@ -236,7 +236,7 @@ fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales
  *   nonfinite_flag  as quantize_act_per_token_group (set if x holds NaN/Inf; nullable).
  *   workspace / workspace_bytes: at least fp8_linear_dynamic_workspace_size(m, n, k) bytes,
  *     256-byte aligned, ZERO-FILLED before first use (the GEMM's split-K counters; every launch
- *     leaves them zeroed).  Decode sizes (1 <= m <= 64 where the decode kernel applies) run ONE
+ *     leaves them zeroed).  Decode sizes (1 <= m <= 8, the token counts of per-GPU rollout decode) run ONE
  *     kernel that quantizes the activations itself (no intermediate codes in HBM, no second
  *     launch); their size may be 0, and NULL is then allowed.  Larger m run the two kernels,
  *     the activation codes and scales living in the workspace (FP8Q_EWORKSPACE if missing).

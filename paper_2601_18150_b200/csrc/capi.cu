@@ -1,5 +1,6 @@
 // capi.cu -- the extern "C" boundary declared in include/fp8q.h: argument validation,
 // status codes, dispatch to the sm_100a kernels.  No allocation, no host sync, no exceptions.
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -432,6 +433,11 @@ namespace {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 int64_t act_ld_s(int64_t m) { return (m + 3) / 4 * 4; }
+// The workspace may be shared with fp8_block_gemm calls of other shapes, whose split-K counters
+// (the first 4 KB, "left zeroed") must stay zero: the activation buffers start past them.
+size_t act_codes_offset(int64_t m, int64_t n, int64_t k) {
+    return align_up(std::max<size_t>(fp8q::gemm_workspace_bytes(m, n, k, false), 4096));
+}
 fp8q::GemmArgs linear_args(const void* x_bf16, int64_t ld_x, const uint8_t* b, int64_t ld_b, const float* b_scales,
                            int64_t ld_sb, void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
                            int64_t k, int32_t* flag) {
@@ -459,7 +465,7 @@ size_t fp8_linear_dynamic_workspace_size(int64_t m, int64_t n, int64_t k) {
     fp8q::GemmArgs g = linear_args(reinterpret_cast<const void*>(16), k, nullptr, k, nullptr, k / 128, nullptr, n,
                                    FP8Q_OUT_BF16, m, n, k, nullptr);
     if (fp8q::skinny_gemm_applies(g)) return fp8q::skinny_workspace_bytes(m, n, k);  // fused: no act buffers
-    return align_up(fp8q::gemm_workspace_bytes(m, n, k, false)) + align_up(static_cast<size_t>(m * k)) +
+    return act_codes_offset(m, n, k) + align_up(static_cast<size_t>(m * k)) +
            static_cast<size_t>(k / 128) * act_ld_s(m) * 4;
 }
 
@@ -494,8 +500,9 @@ fp8q_status fp8_linear_dynamic(const void* x_bf16, int64_t ld_x, const uint8_t* 
     if (workspace == nullptr || workspace_bytes < fp8_linear_dynamic_workspace_size(m, n, k))
         return FP8Q_EWORKSPACE;
     char* base = static_cast<char*>(workspace);
-    uint8_t* codes = reinterpret_cast<uint8_t*>(base + align_up(gws));
-    float* scales = reinterpret_cast<float*>(base + align_up(gws) + align_up(static_cast<size_t>(m * k)));
+    const size_t off = act_codes_offset(m, n, k);
+    uint8_t* codes = reinterpret_cast<uint8_t*>(base + off);
+    float* scales = reinterpret_cast<float*>(base + off + align_up(static_cast<size_t>(m * k)));
     cudaError_t e = fp8q::launch_act_per_token_group(static_cast<const uint16_t*>(x_bf16), m, k, ld_x, codes, k,
                                                      scales, act_ld_s(m), nonfinite_flag, s);
     if (e != cudaSuccess) return from_cuda(e);

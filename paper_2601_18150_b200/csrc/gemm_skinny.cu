@@ -75,11 +75,15 @@ constexpr int pow2_at_least(int v, int lo) {
     return p;
 }
 
-// XQ (fused activation quantization, M <= 64): the producer stages the k-block's BF16
-// activations (MT x 128, X_BF16 slot per stage) and two quantizer warps write the E4M3 codes
-// (SW128 layout, the X slot) and the per-token scales (the SA slot) that the separate
-// quantize_act_per_token_group launch would have written -- same element map
-// (group_quant.cuh), so the GEMM's operands and result are bit-identical.
+// XQ (fused activation quantization, M <= 8): the producer loads each k-block's BF16
+// activations (8 token rows x 128 channels, 2 KB) with its weight tile, and two quantizer warps
+// write the E4M3 codes (SW128 layout, the stage's X slot; rows 8..15 of the MMA's N = 16 are
+// zero) and per-token scales (its SA slot) that the separate quantize_act_per_token_group launch
+// would have written -- same element map (group_quant.cuh), so the GEMM's operands and result
+// are bit-identical.  A 10 % larger budget keeps the weight ring at the unfused depth (5 stages:
+// two CTAs per SM still fit).  (Measured alternatives: a 16-row activation slot per stage cost a
+// weight stage, a 2-slot activation ring owned by the quantizer warps was bound by its TMA round
+// trip: both 25-50 % slower than the unfused GEMM.)
 template <int MT, bool L = (MT <= 32), bool XQ = false>
 struct SkCfg {
     static constexpr int W_TILE = SK_BN * SK_BK;   // 16 KB
@@ -87,14 +91,15 @@ struct SkCfg {
     static constexpr int SA_BYTES = MT * 4;                          // TMA box bytes
     static constexpr int SA_SLOT = SA_BYTES < 128 ? 128 : SA_BYTES;  // TMA smem dst: 128-B aligned
     static constexpr bool XQUANT = XQ;
-    static constexpr int XB_TILE = XQ ? MT * SK_BK * 2 : 0;  // BF16 activation staging
+    static constexpr int XR = 8;                                // XQ: live token rows staged
+    static constexpr int XB_TILE = XQ ? XR * SK_BK * 2 : 0;     // XQ: BF16 activations per stage
     static constexpr int STAGE_BYTES = W_TILE + X_TILE;
     static constexpr int TX_BYTES = XQ ? W_TILE + XB_TILE : STAGE_BYTES + SA_BYTES;  // TMA bytes per stage
     // MT <= 32: half the smem, registers and TMEM, so two CTAs -- this GEMM's and the next
     // one's (programmatic dependent launch) -- fit on an SM and the next GEMM's weight stream
     // starts while this one drains
     static constexpr bool LIGHT = L;
-    static constexpr int BUDGET = LIGHT ? SK_SMEM_BUDGET / 2 : SK_SMEM_BUDGET;
+    static constexpr int BUDGET = LIGHT ? (XQ ? 110 * 1024 : SK_SMEM_BUDGET / 2) : SK_SMEM_BUDGET;
     static constexpr int STAGES_RAW = BUDGET / (STAGE_BYTES + XB_TILE + SA_SLOT);
     static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
     static constexpr int NBUF_RAW = 512 / MT;
@@ -103,6 +108,7 @@ struct SkCfg {
     static constexpr int COLS = MT / 2;  // token columns per promotion thread
     static constexpr uint32_t IDESC = idesc_e4m3_f32(SK_BN, MT);
     static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * (STAGE_BYTES + XB_TILE + SA_SLOT) + 640;
+    static_assert(!XQ || MT == 16, "fused activation quantization: M <= 8 (MMA N = 16)");
     static_assert(MT % 16 == 0 && MT >= 16 && MT <= 256, "MMA N for M=128 must be a multiple of 16, <= 256");
     static_assert(X_TILE % 1024 == 0, "X tile must be whole 128-byte-swizzle atoms");
     // cluster split-K parks its partial in the (contiguous) W and X rings
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* smW = smem;
     uint8_t* smX = smW + STAGES * C::W_TILE;
-    uint8_t* smXb = smX + STAGES * C::X_TILE;  // XQ: BF16 activations (MT rows x 256 B)
+    uint8_t* smXb = smX + STAGES * C::X_TILE;  // XQ: BF16 activations, 8 rows x 256 B per stage
     float* smS = reinterpret_cast<float*>(smXb + STAGES * C::XB_TILE);
     uint64_t* full = reinterpret_cast<uint64_t*>(smS + STAGES * SA_STRIDE);
     uint64_t* empty = full + STAGES;    // the MMA consumed W and X of the stage
@@ -371,13 +377,19 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
-                    mbar_wait(&full[stage], ph);
+                    mbar_wait(&full[stage], ph);  // W and the 8 activation rows landed
                     const uint32_t xb = smem_u32(smXb + stage * C::XB_TILE);
                     const uint32_t xc = smem_u32(smX + stage * C::X_TILE);
-                    float* ss = smS + stage * SA_STRIDE;
+                    const uint32_t ss = smem_u32(smS + stage * SA_STRIDE);
 #pragma unroll 1
                     for (int t0 = 0; t0 < MT; t0 += 8) {
                         const int t = t0 + qw * 4 + (lane >> 3);
+                        const uint32_t dst = xc + static_cast<uint32_t>(t * 128 + ((c ^ (t & 7)) << 4));
+                        if (t0 >= C::XR) {  // rows past the staged 8 (and past m): zero codes, scale 1
+                            st_shared_v4(dst, 0u, 0u, 0u, 0u);
+                            if (c == 0) asm volatile("st.shared.f32 [%0], %1;" ::"r"(ss + 4u * t), "f"(1.0f));
+                            continue;
+                        }
                         uint32_t w[8];
                         const uint32_t src = xb + static_cast<uint32_t>(t * 256 + c * 32);
                         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -387,19 +399,22 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                         uint32_t ab = abs_max_bits16(w);
 #pragma unroll
                         for (int off = 4; off >= 1; off >>= 1) ab = max(ab, __shfl_xor_sync(0xFFFFFFFFu, ab, off));
-                        const bool fast = ab >= kAmaxFastGuardBits && ab < kNonFiniteBits;
-                        float sc, rc = 0.0f;
-                        if (fast)
-                            table_scale_rcp(tabs.t, ab, sc, rc);
-                        else
-                            sc = scale_from_amax_bits(ab);
+                        // all-zero groups (e.g. tokens past m in a partly live pass): s = 1 and the
+                        // Markstein path gives the division path's bytes (+-0 -> 0x00 / 0x80)
+                        const bool fast = (ab >= kAmaxFastGuardBits && ab < kNonFiniteBits) || ab == 0u;
+                        float sc = 1.0f, rc = 1.0f;
+                        if (ab != 0u) {
+                            if (fast)
+                                table_scale_rcp(tabs.t, ab, sc, rc);
+                            else
+                                sc = scale_from_amax_bits(ab);
+                        }
                         if (c == 0) {
-                            ss[t] = sc;
+                            asm volatile("st.shared.f32 [%0], %1;" ::"r"(ss + 4u * t), "f"(sc));
                             if (ab >= kNonFiniteBits && p.flag != nullptr && t < p.m) *p.flag = 1;
                         }
                         const uint4 code = fast ? encode16<true>(w, sc, rc) : encode16<false>(w, sc, 0.0f);
-                        st_shared_v4(xc + static_cast<uint32_t>(t * 128 + ((c ^ (t & 7)) << 4)), code.x, code.y,
-                                     code.z, code.w);
+                        st_shared_v4(dst, code.x, code.y, code.z, code.w);
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
@@ -683,8 +698,6 @@ cudaError_t sk_device_info(int& sms) {
                              static_cast<int>(SkCfg<MT, L, true>::SMEM_BYTES));                                \
     if (e != cudaSuccess) return e;
         SK_ATTR_XQ(16, true)
-        SK_ATTR_XQ(32, true)
-        SK_ATTR_XQ(64, false)
 #undef SK_ATTR_XQ
         di.attr_set = true;
     }
@@ -757,7 +770,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
         // tokens past m zero-filled (their codes are 0 and scales 1: never stored)
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.m)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_a_bf16 * 2)};
-        cuuint32_t box[2] = {SK_BK, MT};
+        cuuint32_t box[2] = {SK_BK, 8};  // SkCfg::XR live rows
         cuuint32_t estr[2] = {1, 1};
         if (encode(&tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(a.a_bf16), dims, strides, box,
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -810,7 +823,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
         grid = static_cast<unsigned>(sk_grid(p.tiles, p.num_kb, sms));
     }
     int cs = 0;
-    if constexpr (MT <= kSkinnyMaxXQ) {
+    if constexpr (MT == 16) {
         cs = xq ? sk_cluster_size<MT, true>(p.tiles, p.num_kb, sms) : sk_cluster_size<MT>(p.tiles, p.num_kb, sms);
     } else {
         cs = sk_cluster_size<MT>(p.tiles, p.num_kb, sms);
@@ -827,10 +840,17 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     // PDL while this one drains), in every mode.  (Round 1 measured the full ring in cluster
     // mode: qkv 11.6 -> 10.9 us but o_proj 7.9 -> 8.5 us per GEMM at M = 1; not adopted.)
     constexpr bool light = MT <= 32;
-    if constexpr (MT <= kSkinnyMaxXQ)
+    // dev A/B: FP8Q_SKINNY_RING=full runs the unfused M <= 32 launches with the full ring
+    static const bool ring_full = [] {
+        const char* e = std::getenv("FP8Q_SKINNY_RING");
+        return e != nullptr && e[0] == 'f';
+    }();
+    const bool use_full = light && ring_full && !xq;
+    if constexpr (MT == 16)
         cfg.dynamicSmemBytes = xq ? SkCfg<MT, light, true>::SMEM_BYTES : SkCfg<MT, light>::SMEM_BYTES;
     else
         cfg.dynamicSmemBytes = SkCfg<MT, light>::SMEM_BYTES;
+    if (use_full) cfg.dynamicSmemBytes = SkCfg<MT, false>::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -841,11 +861,12 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if constexpr (MT <= kSkinnyMaxXQ) {
+    if constexpr (MT == 16) {
         if (xq) return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, light, true>, tmW, tmX, tmS, p);
     } else {
         if (xq) return cudaErrorInvalidValue;
     }
+    if (use_full) return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, false>, tmW, tmX, tmS, p);
     return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, light>, tmW, tmX, tmS, p);
 }
 

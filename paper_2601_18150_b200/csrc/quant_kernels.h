@@ -74,7 +74,7 @@ struct GemmArgs {
     int64_t ld_a_bf16 = 0;
     int32_t* flag = nullptr;  // non-finite activation flag of the fused quantization
 };
-constexpr int kSkinnyMaxXQ = 64;
+constexpr int kSkinnyMaxXQ = 8;
 
 // Decode-sized dense GEMMs (1 <= m <= kSkinnyMaxM) run the swap-AB kernel of gemm_skinny.cu
 // (m > 128 only where its cluster split-K mode applies).
