@@ -839,18 +839,13 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     // M <= 32: the half-budget config (two CTAs per SM, so the next GEMM's CTAs start under
     // PDL while this one drains), in every mode.  (Round 1 measured the full ring in cluster
     // mode: qkv 11.6 -> 10.9 us but o_proj 7.9 -> 8.5 us per GEMM at M = 1; not adopted.)
+    // (Round 2 re-measured the full ring for every M <= 32 mode, and weight tiles issued two
+    // k-blocks at a time: neither faster; the per-CTA stream is not bound by bytes in flight.)
     constexpr bool light = MT <= 32;
-    // dev A/B: FP8Q_SKINNY_RING=full runs the unfused M <= 32 launches with the full ring
-    static const bool ring_full = [] {
-        const char* e = std::getenv("FP8Q_SKINNY_RING");
-        return e != nullptr && e[0] == 'f';
-    }();
-    const bool use_full = light && ring_full && !xq;
     if constexpr (MT == 16)
         cfg.dynamicSmemBytes = xq ? SkCfg<MT, light, true>::SMEM_BYTES : SkCfg<MT, light>::SMEM_BYTES;
     else
         cfg.dynamicSmemBytes = SkCfg<MT, light>::SMEM_BYTES;
-    if (use_full) cfg.dynamicSmemBytes = SkCfg<MT, false>::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -866,7 +861,6 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     } else {
         if (xq) return cudaErrorInvalidValue;
     }
-    if (use_full) return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, false>, tmW, tmX, tmS, p);
     return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, light>, tmW, tmX, tmS, p);
 }
 
