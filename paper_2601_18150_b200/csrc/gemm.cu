@@ -643,7 +643,6 @@ template <int PBN>
 struct PairCfg {
     static constexpr int BN = PBN;          // tile columns
     static constexpr int B_HALF = PBN / 2;  // B rows loaded by each CTA
-    static constexpr int B_BOX = PBN / 2;   // B rows per TMA box
     static constexpr int STAGE_BYTES = A_TILE + B_HALF * BK;  // per CTA
     static constexpr int STAGES = SMEM_BUDGET / STAGE_BYTES;
     static constexpr int NBUF = TMEM_COLS / PBN;

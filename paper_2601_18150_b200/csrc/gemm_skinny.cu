@@ -67,7 +67,6 @@ static_assert(128 * (168 - SK_REGS_CTRL) >= 256 * (SK_REGS_EPI - 168), "register
 constexpr int SK_EPI_WARPS = 8;
 constexpr int SK_SMEM_BUDGET = 200 * 1024;
 constexpr size_t SK_COUNTER_BYTES = 4096;  // one int32 per tile: up to 1024 tiles (N <= 131072)
-constexpr int SK_MAX_SPLITS = 16;
 
 constexpr int pow2_at_least(int v, int lo) {
     int p = lo;
@@ -90,7 +89,6 @@ struct SkCfg {
     static constexpr int X_TILE = MT * SK_BK;      // MT x 128 B (a multiple of 1024 B: SW128 atoms)
     static constexpr int SA_BYTES = MT * 4;                          // TMA box bytes
     static constexpr int SA_SLOT = SA_BYTES < 128 ? 128 : SA_BYTES;  // TMA smem dst: 128-B aligned
-    static constexpr bool XQUANT = XQ;
     static constexpr int XR = 8;                                // XQ: live token rows staged
     static constexpr int XB_TILE = XQ ? XR * SK_BK * 2 : 0;     // XQ: BF16 activations per stage
     static constexpr int STAGE_BYTES = W_TILE + X_TILE;
@@ -202,16 +200,6 @@ __device__ __forceinline__ void tmem_ld_cols<16>(uint32_t taddr, float (&v)[16])
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
-template <>
-__device__ __forceinline__ void tmem_ld_cols<32>(uint32_t taddr, float (&v)[32]) {
-    tmem_ld_32x32b_x32(taddr, v);
-}
-template <>
-__device__ __forceinline__ void tmem_ld_cols<64>(uint32_t taddr, float (&v)[64]) {
-    tmem_ld_32x32b_x32(taddr, *reinterpret_cast<float(*)[32]>(&v[0]));
-    tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<float(*)[32]>(&v[32]));
-}
-
 // D[j0 + j][n_row] for j < jn (a running pointer: not COLS precomputed 64-bit addresses).
 template <int COLS>
 __device__ __forceinline__ void sk_store(const SkParams& p, int64_t n_row, int j0, int jn, const float (&acc)[COLS]) {

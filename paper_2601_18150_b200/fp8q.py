@@ -16,7 +16,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfp8q.so")
+# FP8Q_LIB (dev A/B only): load another build of the same library
+LIB_PATH = os.environ.get("FP8Q_LIB") or os.path.join(_HERE, "libfp8q.so")
 
 FP8Q_OUT_BF16 = 0
 FP8Q_OUT_F32 = 1
