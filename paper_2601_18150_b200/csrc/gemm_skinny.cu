@@ -836,8 +836,12 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
         cfg.dynamicSmemBytes = SkCfg<MT, light>::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
+    static const int no_pdl = [] {  // dev A/B: FP8Q_SKINNY_NOPDL=1 launches without PDL
+        const char* e = std::getenv("FP8Q_SKINNY_NOPDL");
+        return (e != nullptr && e[0] == '1') ? 1 : 0;
+    }();
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
     attr[1].id = cudaLaunchAttributeClusterDimension;
     attr[1].val.clusterDim.x = static_cast<unsigned>(p.cs);
     attr[1].val.clusterDim.y = 1;
