@@ -58,6 +58,9 @@ typedef enum { FP8Q_OUT_BF16 = 0, FP8Q_OUT_F32 = 1 } fp8q_out_dtype;
 
 /* Human-readable name of a status code (static storage; never NULL). */
 const char* fp8q_status_string(fp8q_status s);
+/* The CUDA runtime's message for the last cudaError behind an FP8Q_ECUDA returned on this thread
+ * ("no error" if none): diagnostics only. */
+const char* fp8q_last_cuda_error(void);
 
 /* Library ABI version (major*10000 + minor*100 + patch). */
 int32_t fp8q_version(void);

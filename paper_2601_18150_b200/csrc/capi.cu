@@ -31,11 +31,17 @@ fp8q_status check_device() {
     return c == 1 ? FP8Q_OK : FP8Q_EUNSUPPORTED;
 }
 
-fp8q_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FP8Q_OK : FP8Q_ECUDA; }
+thread_local cudaError_t g_last_cuda = cudaSuccess;
+fp8q_status from_cuda(cudaError_t e) {
+    if (e != cudaSuccess) g_last_cuda = e;
+    return e == cudaSuccess ? FP8Q_OK : FP8Q_ECUDA;
+}
 
 }  // namespace
 
 extern "C" {
+
+const char* fp8q_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda); }
 
 const char* fp8q_status_string(fp8q_status s) {
     switch (s) {
@@ -117,7 +123,7 @@ fp8q_status quantize_weight_blockwise_batched(const fp8q_weight_tensor* tensors,
                                     t.scales, t.ld_s};
         }
         cudaError_t e = fp8q::launch_weight_blockwise_batch(d, c, nonfinite_flag, static_cast<cudaStream_t>(stream));
-        if (e != cudaSuccess) return FP8Q_ECUDA;
+        if (e != cudaSuccess) return from_cuda(e);
         g_launches.fetch_add(fp8q::weight_batch_launches(d, c));
     }
     return FP8Q_OK;
@@ -154,7 +160,7 @@ fp8q_status quantize_weight_blockwise_fanout(const fp8q_weight_tensor* tensors, 
         }
         cudaError_t e = fp8q::launch_weight_blockwise_batch(d, c, nonfinite_flag, static_cast<cudaStream_t>(stream),
                                                             num_dest, codes_delta, scales_delta);
-        if (e != cudaSuccess) return FP8Q_ECUDA;
+        if (e != cudaSuccess) return from_cuda(e);
         g_launches.fetch_add(fp8q::weight_batch_launches(d, c));
     }
     return FP8Q_OK;

@@ -48,7 +48,9 @@ constexpr int EPI_WARP0 = 4;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int RASTER_GM = 16;  // m-tiles per raster band
-constexpr int SMEM_BUDGET = 160 * 1024;  // operand stages
+// operand stages: 160 KB + the 64 KB BF16 epilogue staging + barriers + alignment slack = the
+// 227 KB per-CTA limit (a 6th pair stage does not fit: measured, launch rejected)
+constexpr int SMEM_BUDGET = 160 * 1024;
 // Output staging for the TMA-store epilogue: per promotion warp four 32-row x 64-byte
 // chunks (2 KB each, 64-byte swizzle) -> 8 warps x 8 KB.  A BF16 half-tile row segment
 // (128 columns) is exactly 4 chunks, so a tile's stores never wait for each other.
