@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/fp8q.h"
@@ -470,7 +471,9 @@ size_t fp8_linear_dynamic_workspace_size(int64_t m, int64_t n, int64_t k) {
     if (m <= 0 || n <= 0 || k <= 0) return 0;
     fp8q::GemmArgs g = linear_args(reinterpret_cast<const void*>(16), k, nullptr, k, nullptr, k / 128, nullptr, n,
                                    FP8Q_OUT_BF16, m, n, k, nullptr);
-    if (fp8q::skinny_gemm_applies(g)) return fp8q::skinny_workspace_bytes(m, n, k);  // fused: no act buffers
+    const char* fe = std::getenv("FP8Q_LINEAR_FUSED");
+    const bool fused_off = fe != nullptr && fe[0] == '0';
+    if (!fused_off && fp8q::skinny_gemm_applies(g)) return fp8q::skinny_workspace_bytes(m, n, k);  // fused
     return act_codes_offset(m, n, k) + align_up(static_cast<size_t>(m * k)) +
            static_cast<size_t>(k / 128) * act_ld_s(m) * 4;
 }
@@ -493,7 +496,11 @@ fp8q_status fp8_linear_dynamic(const void* x_bf16, int64_t ld_x, const uint8_t* 
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     fp8q::GemmArgs g = linear_args(x_bf16, ld_x, b, ld_b, b_scales, ld_sb, d, ld_d, d_dtype, m, n, k,
                                    nonfinite_flag);
-    if (fp8q::skinny_gemm_applies(g)) {  // decode sizes: one launch, activations quantized in the GEMM
+    static const bool fused_off = [] {  // dev A/B: FP8Q_LINEAR_FUSED=0 always runs the two launches
+        const char* e = std::getenv("FP8Q_LINEAR_FUSED");
+        return e != nullptr && e[0] == '0';
+    }();
+    if (!fused_off && fp8q::skinny_gemm_applies(g)) {  // decode sizes: one launch, activations quantized in the GEMM
         g.workspace = workspace;
         g.workspace_bytes = workspace_bytes;
         int launched = 0;

@@ -22,6 +22,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <utility>
 
 #include "ptx.cuh"
 #include "quant_kernels.h"
@@ -32,6 +33,29 @@
 namespace fp8q {
 
 namespace {
+
+// Programmatic dependent launch (the activation quantizers run between a GEMM producing their
+// input and the GEMM consuming their output): trigger the dependent launch early, and wait for
+// the preceding grid (complete + its memory visible) before touching x, codes or scales.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Launch with the programmatic-stream-serialization attribute (PDL).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // RN32(x / s) for blocks with amax >= 2^-104 (see header comment), sign taken from x.
 __device__ __forceinline__ float quot_fast(float x, float s, float r) {
@@ -393,8 +417,10 @@ __global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
     float* __restrict__ scales, int64_t ld_s, int64_t groups, int64_t chunks, int64_t items,
     int32_t* __restrict__ nonfinite_flag) {
     __shared__ ScaleTables tabs;
+    pdl_launch_dependents();  // the consumer GEMM may start its weight prefetch now
     init_scale_tables(tabs);
     __syncthreads();
+    pdl_wait();  // x is the previous kernel's output; q / scales may still be read by it
     const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
     int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     AItemRegs a, b;
@@ -478,6 +504,7 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
     const __grid_constant__ ABatch ab, int32_t* __restrict__ nonfinite_flag) {
     extern __shared__ __align__(128) uint8_t abq_smem[];
     __shared__ ScaleTables tabs;
+    pdl_launch_dependents();
     uint64_t* full = reinterpret_cast<uint64_t*>(abq_smem + size_t(ABQ_STAGES) * ABQ_ITEMS * ABQ_ITEM_BYTES);
     uint64_t* empty = full + ABQ_STAGES;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -499,6 +526,7 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_wait();  // (no-op unless launched with programmatic stream serialization)
     const uint32_t ring = smem_u32(abq_smem);
     if (warp == ABQ_ITEMS * ABQ_TEAMS) {
         if (lane == 0 && i1 > i0) {
@@ -885,8 +913,9 @@ cudaError_t launch_act_unstaged(const ActDesc& d, int32_t* flag, cudaStream_t st
         const int64_t witems = d.m * wchunks;
         const int64_t wblocks = (witems + 7) / 8;
         const int64_t grid = wblocks < 2LL * sm_count() ? wblocks : 2LL * sm_count();
-        act_per_token_group_wide_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(
-            d.x, d.ld_x, d.q, d.ld_q, d.scales, d.ld_s, groups, wchunks, witems, flag);
+        const cudaError_t e = launch_pdl(act_per_token_group_wide_kernel, static_cast<unsigned>(grid), 256, 0, stream,
+                                         d.x, d.ld_x, d.q, d.ld_q, d.scales, d.ld_s, groups, wchunks, witems, flag);
+        if (e != cudaSuccess) return e;
     } else {
         const int64_t chunks = (groups + 7) / 8;
         const int64_t blocks = (d.m * chunks + 7) / 8;
@@ -902,7 +931,7 @@ int act_batch_launches(const ActDesc* descs, int count) {
     int staged = 0, other = 0;
     for (int i = 0; i < count; ++i) {
         if (descs[i].m == 0 || descs[i].k == 0) continue;
-        if (act_kernel_env() == 0 && act_staged_ok(descs[i])) ++staged; else ++other;
+        if (act_kernel_env() == 0 && act_staged_ok(descs[i]) && descs[i].m > 256) ++staged; else ++other;
     }
     return other + (staged + kMaxActBatch - 1) / kMaxActBatch;
 }
@@ -939,12 +968,12 @@ cudaError_t launch_act_batch(const ActDesc* descs, int count, int32_t* flag, cud
         const int64_t per_cta_min = 2 * ABQ_ITEMS;  // small inputs: fewer CTAs, each a few stages
         int64_t grid = (ab.items + per_cta_min - 1) / per_cta_min;
         grid = grid < sm_count() ? grid : sm_count();
-        if (use_tma)
-            act_per_token_group_bulk_kernel<true><<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
-                ab, flag);
-        else
-            act_per_token_group_bulk_kernel<false><<<static_cast<unsigned>(grid), ABQ_THREADS, ABQ_SMEM, stream>>>(
-                ab, flag);
+        const cudaError_t e =
+            use_tma ? launch_pdl(act_per_token_group_bulk_kernel<true>, static_cast<unsigned>(grid), ABQ_THREADS,
+                                 ABQ_SMEM, stream, ab, flag)
+                    : launch_pdl(act_per_token_group_bulk_kernel<false>, static_cast<unsigned>(grid), ABQ_THREADS,
+                                 ABQ_SMEM, stream, ab, flag);
+        if (e != cudaSuccess) return e;
         ab.count = 0;
         ab.items = 0;
         return cudaGetLastError();
@@ -952,7 +981,10 @@ cudaError_t launch_act_batch(const ActDesc* descs, int count, int32_t* flag, cud
     for (int i = 0; i < count; ++i) {
         const ActDesc& d = descs[i];
         if (d.m == 0 || d.k == 0) continue;
-        if (act_kernel_env() != 0 || !act_staged_ok(d)) {
+        // decode-sized inputs (<= 256 tokens) take the register path: no shared memory, so under
+        // PDL its CTAs fit beside the previous GEMM's and the quantization starts the moment
+        // that GEMM retires
+        if (act_kernel_env() != 0 || !act_staged_ok(d) || d.m <= 256) {
             cudaError_t e = launch_act_unstaged(d, flag, stream);
             if (e != cudaSuccess) return e;
             continue;

@@ -59,7 +59,8 @@ def load_library() -> ctypes.CDLL:
         lib.fp8q_status_string.argtypes = [ctypes.c_int]
         lib.fp8q_status_string.restype = ctypes.c_char_p
         lib.fp8q_version.restype = I32
-        lib.fp8q_last_cuda_error.restype = ctypes.c_char_p
+        if hasattr(lib, "fp8q_last_cuda_error"):  # (older builds loaded via FP8Q_LIB lack it)
+            lib.fp8q_last_cuda_error.restype = ctypes.c_char_p
         lib.fp8q_kernel_launches.restype = I64
         lib.quantize_weight_blockwise.argtypes = [P, I64, I64, I64, P, I64, P, I64, P, P]
         lib.quantize_weight_blockwise.restype = ctypes.c_int
@@ -114,7 +115,7 @@ def _check(status: int, what: str) -> None:
     if status != 0:
         lib = load_library()
         msg = lib.fp8q_status_string(status).decode()
-        if msg == "FP8Q_ECUDA" or "ECUDA" in msg:
+        if "ECUDA" in msg and hasattr(lib, "fp8q_last_cuda_error"):
             msg += f" ({lib.fp8q_last_cuda_error().decode()})"
         raise Fp8qError(f"{what}: {msg}")
 

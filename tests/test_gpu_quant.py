@@ -272,7 +272,11 @@ def test_act_batched_matches_oracle(shapes):
     before = fp8q.kernel_launches()
     fp8q.quantize_act_per_token_group_batched(items)
     torch.cuda.synchronize()
-    assert fp8q.kernel_launches() - before == (len([s for s in shapes if s[0]]) + 7) // 8
+    # tensors of > 256 tokens share persistent staged launches (8 per launch); decode-sized ones
+    # (<= 256 tokens) each take the register kernel (PDL-friendly: no shared memory)
+    staged = len([s for s in shapes if s[0] > 256])
+    small = len([s for s in shapes if 0 < s[0] <= 256])
+    assert fp8q.kernel_launches() - before == small + (staged + 7) // 8
     for (m, k), (x, codes, scales), r in zip(shapes, items, ref):
         if not m:
             continue
