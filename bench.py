@@ -396,7 +396,7 @@ def bench_decode(st: LayerStep, peaks, clocks, ms=(1, 64, 128, 256), copies=4, r
 
         def layer(c, s, which=None):
             # each linear as the rollout engine calls it: BF16 input, dynamic activation
-            # quantization + blockwise FP8 GEMM (one fused kernel at M <= 8, two launches above)
+            # quantization + blockwise FP8 GEMM, chained by programmatic dependent launch)
             for nm, _, _ in LAYER:
                 if which is None or nm == which:
                     fq.fp8_linear_dynamic(xs[nm], c[nm], s[nm], out=ys[nm])
@@ -443,7 +443,7 @@ def bench_decode(st: LayerStep, peaks, clocks, ms=(1, 64, 128, 256), copies=4, r
     del layers
     return {"config": "BASELINE.json configs[2]: Qwen3-8B decode-shaped GEMMs (M tokens, real N, K), bf16 out; "
                       "each linear = fp8_linear_dynamic (BF16 input quantized per token per 128 channels + "
-                      "blockwise FP8 GEMM: one fused kernel at M <= 8, two launches above)",
+                      "blockwise FP8 GEMM, two kernels chained by programmatic dependent launch)",
             "timing": f"one CUDA graph of {copies} layers x 4 replays (weights rotate over {copies} copies, "
                       f"{copies} x 193 MB > L2), median of {replays} replays; per_gemm = graphs of one linear "
                       "(incl. its activation quantization) alone",

@@ -239,10 +239,11 @@ fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales
  *   nonfinite_flag  as quantize_act_per_token_group (set if x holds NaN/Inf; nullable).
  *   workspace / workspace_bytes: at least fp8_linear_dynamic_workspace_size(m, n, k) bytes,
  *     256-byte aligned, ZERO-FILLED before first use (the GEMM's split-K counters; every launch
- *     leaves them zeroed).  Decode sizes (1 <= m <= 8, the token counts of per-GPU rollout decode) run ONE
- *     kernel that quantizes the activations itself (no intermediate codes in HBM, no second
- *     launch); their size may be 0, and NULL is then allowed.  Larger m run the two kernels,
- *     the activation codes and scales living in the workspace (FP8Q_EWORKSPACE if missing).
+ *     leaves them zeroed), holding the activation codes and scales between the two kernels
+ *     (FP8Q_EWORKSPACE if missing or too small).  The quantizer is launched with programmatic
+ *     dependent launch and, for <= 256 tokens, as a shared-memory-free kernel, so the decode
+ *     GEMM's weight prefetch overlaps it.  (Round 2 also built a single-kernel form -- the decode
+ *     GEMM quantizing its activations itself: slower than this pair, removed.)
  *   Requirements as fp8_block_gemm (k % 128, n % 8, alignments).
  */
 size_t fp8_linear_dynamic_workspace_size(int64_t m, int64_t n, int64_t k);

@@ -434,8 +434,8 @@ fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales
     return from_cuda(e);
 }
 
-// fp8_linear_dynamic: workspace = [GEMM split-K workspace][activation codes m x k][scales];
-// the fused decode kernel needs none of the last two.
+// fp8_linear_dynamic: quantize_act_per_token_group into the workspace, then fp8_block_gemm;
+// workspace = [GEMM split-K workspace, at least the 4 KB of counters][codes m x k][scales].
 namespace {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
@@ -445,35 +445,10 @@ int64_t act_ld_s(int64_t m) { return (m + 3) / 4 * 4; }
 size_t act_codes_offset(int64_t m, int64_t n, int64_t k) {
     return align_up(std::max<size_t>(fp8q::gemm_workspace_bytes(m, n, k, false), 4096));
 }
-fp8q::GemmArgs linear_args(const void* x_bf16, int64_t ld_x, const uint8_t* b, int64_t ld_b, const float* b_scales,
-                           int64_t ld_sb, void* d, int64_t ld_d, fp8q_out_dtype d_dtype, int64_t m, int64_t n,
-                           int64_t k, int32_t* flag) {
-    fp8q::GemmArgs g{};
-    g.b = b;
-    g.ld_b = ld_b;
-    g.sb = b_scales;
-    g.ld_sb = ld_sb;
-    g.d = d;
-    g.ld_d = ld_d;
-    g.out_f32 = d_dtype == FP8Q_OUT_F32;
-    g.m = m;
-    g.n = n;
-    g.k = k;
-    g.groups = 1;
-    g.a_bf16 = static_cast<const uint16_t*>(x_bf16);
-    g.ld_a_bf16 = ld_x;
-    g.flag = flag;
-    return g;
-}
 }  // namespace
 
 size_t fp8_linear_dynamic_workspace_size(int64_t m, int64_t n, int64_t k) {
     if (m <= 0 || n <= 0 || k <= 0) return 0;
-    fp8q::GemmArgs g = linear_args(reinterpret_cast<const void*>(16), k, nullptr, k, nullptr, k / 128, nullptr, n,
-                                   FP8Q_OUT_BF16, m, n, k, nullptr);
-    const char* fe = std::getenv("FP8Q_LINEAR_FUSED");
-    const bool fused_off = fe != nullptr && fe[0] == '0';
-    if (!fused_off && fp8q::skinny_gemm_applies(g)) return fp8q::skinny_workspace_bytes(m, n, k);  // fused
     return act_codes_offset(m, n, k) + align_up(static_cast<size_t>(m * k)) +
            static_cast<size_t>(k / 128) * act_ld_s(m) * 4;
 }
@@ -493,39 +468,35 @@ fp8q_status fp8_linear_dynamic(const void* x_bf16, int64_t ld_x, const uint8_t* 
     if (k > 0 && (!aligned(x_bf16, 16) || ld_x % 8 != 0)) return FP8Q_EALIGN;
     if (nonfinite_flag != nullptr && !aligned(nonfinite_flag, 4)) return FP8Q_EALIGN;
     if (k == 0) return zero_output(d, ld_d, d_dtype, m, n, stream);
+    if (workspace == nullptr || workspace_bytes < fp8_linear_dynamic_workspace_size(m, n, k)) return FP8Q_EWORKSPACE;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    fp8q::GemmArgs g = linear_args(x_bf16, ld_x, b, ld_b, b_scales, ld_sb, d, ld_d, d_dtype, m, n, k,
-                                   nonfinite_flag);
-    static const bool fused_off = [] {  // dev A/B: FP8Q_LINEAR_FUSED=0 always runs the two launches
-        const char* e = std::getenv("FP8Q_LINEAR_FUSED");
-        return e != nullptr && e[0] == '0';
-    }();
-    if (!fused_off && fp8q::skinny_gemm_applies(g)) {  // decode sizes: one launch, activations quantized in the GEMM
-        g.workspace = workspace;
-        g.workspace_bytes = workspace_bytes;
-        int launched = 0;
-        const cudaError_t e = fp8q::launch_fp8_block_gemm(g, s, &launched);
-        g_launches.fetch_add(launched);
-        return from_cuda(e);
-    }
-    // otherwise: quantize_act_per_token_group into the workspace, then fp8_block_gemm
     const size_t gws = fp8q::gemm_workspace_bytes(m, n, k, false);
-    if (workspace == nullptr || workspace_bytes < fp8_linear_dynamic_workspace_size(m, n, k))
-        return FP8Q_EWORKSPACE;
     char* base = static_cast<char*>(workspace);
     const size_t off = act_codes_offset(m, n, k);
     uint8_t* codes = reinterpret_cast<uint8_t*>(base + off);
     float* scales = reinterpret_cast<float*>(base + off + align_up(static_cast<size_t>(m * k)));
+    // (the quantizer is launched with programmatic dependent launch, the decode GEMM too: the
+    // GEMM's weight prefetch overlaps the quantization)
     cudaError_t e = fp8q::launch_act_per_token_group(static_cast<const uint16_t*>(x_bf16), m, k, ld_x, codes, k,
                                                      scales, act_ld_s(m), nonfinite_flag, s);
     if (e != cudaSuccess) return from_cuda(e);
     g_launches.fetch_add(1);
-    g.a_bf16 = nullptr;
-    g.flag = nullptr;
+    fp8q::GemmArgs g{};
     g.a = codes;
     g.ld_a = k;
     g.sa = scales;
     g.ld_sa = act_ld_s(m);
+    g.b = b;
+    g.ld_b = ld_b;
+    g.sb = b_scales;
+    g.ld_sb = ld_sb;
+    g.d = d;
+    g.ld_d = ld_d;
+    g.out_f32 = d_dtype == FP8Q_OUT_F32;
+    g.m = m;
+    g.n = n;
+    g.k = k;
+    g.groups = 1;
     g.workspace = gws > 0 ? workspace : nullptr;
     g.workspace_bytes = gws;
     int launched = 0;

@@ -47,10 +47,8 @@
 #include <cstdlib>
 #include <mutex>
 
-#include "group_quant.cuh"
 #include "ptx.cuh"
 #include "quant_kernels.h"
-#include "scale_tables.cuh"
 
 namespace fp8q {
 namespace {
@@ -74,39 +72,27 @@ constexpr int pow2_at_least(int v, int lo) {
     return p;
 }
 
-// XQ (fused activation quantization, M <= 8): the producer loads each k-block's BF16
-// activations (8 token rows x 128 channels, 2 KB) with its weight tile, and two quantizer warps
-// write the E4M3 codes (SW128 layout, the stage's X slot; rows 8..15 of the MMA's N = 16 are
-// zero) and per-token scales (its SA slot) that the separate quantize_act_per_token_group launch
-// would have written -- same element map (group_quant.cuh), so the GEMM's operands and result
-// are bit-identical.  A 10 % larger budget keeps the weight ring at the unfused depth (5 stages:
-// two CTAs per SM still fit).  (Measured alternatives: a 16-row activation slot per stage cost a
-// weight stage, a 2-slot activation ring owned by the quantizer warps was bound by its TMA round
-// trip: both 25-50 % slower than the unfused GEMM.)
-template <int MT, bool L = (MT <= 32), bool XQ = false>
+template <int MT, bool L = (MT <= 32)>
 struct SkCfg {
     static constexpr int W_TILE = SK_BN * SK_BK;   // 16 KB
     static constexpr int X_TILE = MT * SK_BK;      // MT x 128 B (a multiple of 1024 B: SW128 atoms)
     static constexpr int SA_BYTES = MT * 4;                          // TMA box bytes
     static constexpr int SA_SLOT = SA_BYTES < 128 ? 128 : SA_BYTES;  // TMA smem dst: 128-B aligned
-    static constexpr int XR = 8;                                // XQ: live token rows staged
-    static constexpr int XB_TILE = XQ ? XR * SK_BK * 2 : 0;     // XQ: BF16 activations per stage
     static constexpr int STAGE_BYTES = W_TILE + X_TILE;
-    static constexpr int TX_BYTES = XQ ? W_TILE + XB_TILE : STAGE_BYTES + SA_BYTES;  // TMA bytes per stage
+    static constexpr int TX_BYTES = STAGE_BYTES + SA_BYTES;  // TMA bytes per stage
     // MT <= 32: half the smem, registers and TMEM, so two CTAs -- this GEMM's and the next
     // one's (programmatic dependent launch) -- fit on an SM and the next GEMM's weight stream
     // starts while this one drains
     static constexpr bool LIGHT = L;
-    static constexpr int BUDGET = LIGHT ? (XQ ? 110 * 1024 : SK_SMEM_BUDGET / 2) : SK_SMEM_BUDGET;
-    static constexpr int STAGES_RAW = BUDGET / (STAGE_BYTES + XB_TILE + SA_SLOT);
+    static constexpr int BUDGET = LIGHT ? SK_SMEM_BUDGET / 2 : SK_SMEM_BUDGET;
+    static constexpr int STAGES_RAW = BUDGET / (STAGE_BYTES + SA_SLOT);
     static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
     static constexpr int NBUF_RAW = 512 / MT;
     static constexpr int NBUF = NBUF_RAW > 8 ? 8 : NBUF_RAW;  // TMEM partial buffers
     static constexpr int TMEM_COLS = pow2_at_least(NBUF * MT, 32);
     static constexpr int COLS = MT / 2;  // token columns per promotion thread
     static constexpr uint32_t IDESC = idesc_e4m3_f32(SK_BN, MT);
-    static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * (STAGE_BYTES + XB_TILE + SA_SLOT) + 640;
-    static_assert(!XQ || MT == 16, "fused activation quantization: M <= 8 (MMA N = 16)");
+    static constexpr size_t SMEM_BYTES = 1024 + size_t(STAGES) * (STAGE_BYTES + SA_SLOT) + 512;
     static_assert(MT % 16 == 0 && MT >= 16 && MT <= 256, "MMA N for M=128 must be a multiple of 16, <= 256");
     static_assert(X_TILE % 1024 == 0, "X tile must be whole 128-byte-swizzle atoms");
     // cluster split-K parks its partial in the (contiguous) W and X rings
@@ -127,15 +113,7 @@ struct SkParams {
     int64_t total;      // T = tiles * num_kb
     float* ws;          // stream-K partials: two [MT][128] fp32 slots per CTA
     int32_t* counters;  // [tiles], left zeroed
-    int32_t* flag;      // XQ: non-finite activation flag (nullable)
 };
-template <bool XQ>
-struct SkTabs {
-    ScaleTables t;
-};
-template <>
-struct SkTabs<false> {};
-
 __device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Walks this CTA's segments: (tile, kb0, kb1) = k-blocks [kb0, kb1) of weight tile `tile`.
@@ -220,11 +198,11 @@ __device__ __forceinline__ void sk_store(const SkParams& p, int64_t n_row, int j
     }
 }
 
-template <int MT, bool L, bool XQ = false>
+template <int MT, bool L>
 __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
     fp8_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                            const __grid_constant__ CUtensorMap tmS, const SkParams p) {
-    using C = SkCfg<MT, L, XQ>;
+    using C = SkCfg<MT, L>;
     constexpr int STAGES = C::STAGES;
     constexpr int NBUF = C::NBUF;
     constexpr int COLS = C::COLS;
@@ -234,26 +212,21 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* smW = smem;
     uint8_t* smX = smW + STAGES * C::W_TILE;
-    uint8_t* smXb = smX + STAGES * C::X_TILE;  // XQ: BF16 activations, 8 rows x 256 B per stage
-    float* smS = reinterpret_cast<float*>(smXb + STAGES * C::XB_TILE);
+    float* smS = reinterpret_cast<float*>(smX + STAGES * C::X_TILE);
     uint64_t* full = reinterpret_cast<uint64_t*>(smS + STAGES * SA_STRIDE);
     uint64_t* empty = full + STAGES;    // the MMA consumed W and X of the stage
     uint64_t* sempty = empty + STAGES;  // the promotion warps consumed its activation scales
-    uint64_t* xfull = sempty + STAGES;  // XQ: the quantizer warps wrote the stage's codes + scales
-    uint64_t* tfull = xfull + (XQ ? STAGES : 0);
+    uint64_t* tfull = sempty + STAGES;
     uint64_t* tempty = tfull + NBUF;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    __shared__ SkTabs<XQ> tabs;
-    if constexpr (XQ) init_scale_tables(tabs.t);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
             mbar_init(&sempty[s], SK_EPI_WARPS);
-            if constexpr (XQ) mbar_init(&xfull[s], 2);
         }
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);
@@ -275,7 +248,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
             // ------------------------------------------------------------ TMA producer
             tma_prefetch_desc(&tmW);
             tma_prefetch_desc(&tmX);
-            if constexpr (!XQ) tma_prefetch_desc(&tmS);
+            tma_prefetch_desc(&tmS);
             // Programmatic dependent launch: the weights (and their scales) are never written by
             // the kernel this one may overlap (only this kernel triggers early, see below), so
             // the first ring fill of weight tiles is issued before waiting for the previous
@@ -308,12 +281,8 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                         mbar_arrive_expect_tx(&full[stage], C::TX_BYTES);
                         tma_load_2d(smW + stage * C::W_TILE, &tmW, &full[stage], kb * SK_BK, tile * SK_BN);
                     }
-                    if constexpr (XQ) {
-                        tma_load_2d(smXb + stage * C::XB_TILE, &tmX, &full[stage], kb * SK_BK, 0);
-                    } else {
-                        tma_load_2d(smX + stage * C::X_TILE, &tmX, &full[stage], kb * SK_BK, 0);
-                        tma_load_2d(smS + stage * SA_STRIDE, &tmS, &full[stage], 0, kb);
-                    }
+                    tma_load_2d(smX + stage * C::X_TILE, &tmX, &full[stage], kb * SK_BK, 0);
+                    tma_load_2d(smS + stage * SA_STRIDE, &tmS, &full[stage], 0, kb);
                 }
             }
         }
@@ -333,7 +302,6 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                     const uint32_t bph = (it / NBUF) & 1u;
                     mbar_wait(&tempty[buf], bph ^ 1u);
                     mbar_wait(&full[stage], ph);
-                    if constexpr (XQ) mbar_wait(&xfull[stage], ph);  // codes written by the quantizer warps
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(smW + stage * C::W_TILE);
                     const uint32_t b0 = smem_u32(smX + stage * C::X_TILE);
@@ -344,69 +312,6 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                                    kk > 0 ? 1u : 0u);
                     mma_commit(&empty[stage]);
                     mma_commit(&tfull[buf]);
-                }
-            }
-        }
-    } else if (XQ && (warp == 2 || warp == 3)) {
-        // ---------------------------------------------------------------- quantizer warps (XQ)
-        // Per k-block: MT tokens x 128 channels = MT groups; 8 lanes per group (16 channels
-        // each), 4 groups per warp and pass.  Codes go to the X slot in the layout the TMA's
-        // 128-byte swizzle would give (16-byte chunk c of row t at chunk c ^ (t & 7)), scales
-        // to the SA slot; then an async-proxy fence (the tensor core reads the codes) and one
-        // arrive per warp on xfull.
-        if constexpr (XQ) {
-            const int qw = warp - 2;
-            const int c = lane & 7;
-            uint32_t it = 0;
-            SegIter seg;
-            seg.init(p);
-            int tile, kb0, kb1;
-            while (seg.next(p, tile, kb0, kb1)) {
-                for (int kb = kb0; kb < kb1; ++kb, ++it) {
-                    const uint32_t stage = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1u;
-                    mbar_wait(&full[stage], ph);  // W and the 8 activation rows landed
-                    const uint32_t xb = smem_u32(smXb + stage * C::XB_TILE);
-                    const uint32_t xc = smem_u32(smX + stage * C::X_TILE);
-                    const uint32_t ss = smem_u32(smS + stage * SA_STRIDE);
-#pragma unroll 1
-                    for (int t0 = 0; t0 < MT; t0 += 8) {
-                        const int t = t0 + qw * 4 + (lane >> 3);
-                        const uint32_t dst = xc + static_cast<uint32_t>(t * 128 + ((c ^ (t & 7)) << 4));
-                        if (t0 >= C::XR) {  // rows past the staged 8 (and past m): zero codes, scale 1
-                            st_shared_v4(dst, 0u, 0u, 0u, 0u);
-                            if (c == 0) asm volatile("st.shared.f32 [%0], %1;" ::"r"(ss + 4u * t), "f"(1.0f));
-                            continue;
-                        }
-                        uint32_t w[8];
-                        const uint32_t src = xb + static_cast<uint32_t>(t * 256 + c * 32);
-                        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(src));
-                        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                                     : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "r"(src + 16));
-                        uint32_t ab = abs_max_bits16(w);
-#pragma unroll
-                        for (int off = 4; off >= 1; off >>= 1) ab = max(ab, __shfl_xor_sync(0xFFFFFFFFu, ab, off));
-                        // all-zero groups (e.g. tokens past m in a partly live pass): s = 1 and the
-                        // Markstein path gives the division path's bytes (+-0 -> 0x00 / 0x80)
-                        const bool fast = (ab >= kAmaxFastGuardBits && ab < kNonFiniteBits) || ab == 0u;
-                        float sc = 1.0f, rc = 1.0f;
-                        if (ab != 0u) {
-                            if (fast)
-                                table_scale_rcp(tabs.t, ab, sc, rc);
-                            else
-                                sc = scale_from_amax_bits(ab);
-                        }
-                        if (c == 0) {
-                            asm volatile("st.shared.f32 [%0], %1;" ::"r"(ss + 4u * t), "f"(sc));
-                            if (ab >= kNonFiniteBits && p.flag != nullptr && t < p.m) *p.flag = 1;
-                        }
-                        const uint4 code = fast ? encode16<true>(w, sc, rc) : encode16<false>(w, sc, 0.0f);
-                        st_shared_v4(dst, code.x, code.y, code.z, code.w);
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&xfull[stage]);
                 }
             }
         }
@@ -439,10 +344,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                 const uint32_t buf = it % NBUF;
                 const uint32_t bph = (it / NBUF) & 1u;
                 mbar_wait(&tfull[buf], bph);
-                if constexpr (XQ)
-                    mbar_wait(&xfull[stage], ph);  // orders the quantizer-written scales
-                else
-                    mbar_wait(&full[stage], ph);  // (already complete) orders the TMA-written scales
+                mbar_wait(&full[stage], ph);  // (already complete) orders the TMA-written scales
                 tc_fence_after();
                 const float* sa_s = smS + stage * SA_STRIDE + j0;
                 // chunks of <= 16 columns keep the live registers at acc + one chunk
@@ -681,12 +583,6 @@ cudaError_t sk_device_info(int& sms) {
         SK_ATTR(128, false)
         SK_ATTR(256, false)
 #undef SK_ATTR
-#define SK_ATTR_XQ(MT, L)                                                                                    \
-    e = cudaFuncSetAttribute(fp8_gemm_skinny_kernel<MT, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             static_cast<int>(SkCfg<MT, L, true>::SMEM_BYTES));                                \
-    if (e != cudaSuccess) return e;
-        SK_ATTR_XQ(16, true)
-#undef SK_ATTR_XQ
         di.attr_set = true;
     }
     sms = di.sms;
@@ -697,9 +593,8 @@ cudaError_t sk_device_info(int& sms) {
 // idle: the largest cs <= 8 with tiles * cs <= sms whose clusters are all co-resident
 // (cudaOccupancyMaxActiveClusters: a cluster must fit in one GPC).  0: not applicable.
 // Dev override FP8Q_SKINNY_CLUSTER=0 disables it (stream-K instead).  Cached per shape class.
-template <int MT, bool XQ = false>
+template <int MT>
 int sk_cluster_size(int tiles, int num_kb, int sms) {
-    constexpr bool QL = XQ && MT <= 32;  // the fused variants exist in the launched config only
     static const bool enabled = [] {
         const char* e = std::getenv("FP8Q_SKINNY_CLUSTER");
         return !(e != nullptr && e[0] == '0');
@@ -712,13 +607,12 @@ int sk_cluster_size(int tiles, int num_kb, int sms) {
     std::lock_guard<std::mutex> lk(mu);
     for (int i = 0; i < used; ++i)
         if (cache[i].tiles == tiles && cache[i].num_kb == num_kb && cache[i].sms == sms) return cache[i].cs;
-    // (static locals are per template instance: the cache never mixes MT or XQ)
     int c = std::min(8, std::min(sms / tiles, num_kb / 2));
     for (; c >= 2; --c) {
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3(static_cast<unsigned>(tiles * c));
         q.blockDim = dim3(SK_THREADS);
-        q.dynamicSmemBytes = SkCfg<MT, QL, XQ>::SMEM_BYTES;
+        q.dynamicSmemBytes = SkCfg<MT, false>::SMEM_BYTES;
         cudaLaunchAttribute ca;
         ca.id = cudaLaunchAttributeClusterDimension;
         ca.val.clusterDim.x = static_cast<unsigned>(c);
@@ -727,7 +621,7 @@ int sk_cluster_size(int tiles, int num_kb, int sms) {
         q.attrs = &ca;
         q.numAttrs = 1;
         int active = 0;
-        const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, fp8_gemm_skinny_kernel<MT, QL, XQ>, &q);
+        const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, fp8_gemm_skinny_kernel<MT, false>, &q);
         if (std::getenv("FP8Q_DEBUG_CLUSTER") != nullptr)
             std::fprintf(stderr, "[fp8q] skinny MT=%d tiles=%d kb=%d: cluster %d -> %d active (%s)\n", MT, tiles,
                          num_kb, c, active, cudaGetErrorString(e));
@@ -752,20 +646,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    const bool xq = a.a_bf16 != nullptr;
-    if (xq) {
-        // BF16 activations [m][k] (row stride ld_a_bf16 elements), box 128 channels x MT tokens,
-        // tokens past m zero-filled (their codes are 0 and scales 1: never stored)
-        cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.m)};
-        cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_a_bf16 * 2)};
-        cuuint32_t box[2] = {SK_BK, 8};  // SkCfg::XR live rows
-        cuuint32_t estr[2] = {1, 1};
-        if (encode(&tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(a.a_bf16), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return cudaErrorInvalidValue;
-        tmS = tmX;  // unused by the fused kernel
-    } else {
+    {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.m)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_a)};
         cuuint32_t box[2] = {SK_BK, MT};
@@ -775,7 +656,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    if (!xq) {
+    {
         // activation scales, MN-major [k/128][ld_sa]: row kb holds the m tokens' scales
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.m), static_cast<cuuint64_t>(a.k / SK_BK)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_sa * 4)};
@@ -801,7 +682,6 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     p.cs = 1;
     p.ws = nullptr;
     p.counters = nullptr;
-    p.flag = a.flag;
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, sms));  // whole tiles
     const size_t need = sk_ws_bytes(a.m, a.n, a.k, sms);
     if (need > 0 && a.workspace != nullptr && a.workspace_bytes >= need) {
@@ -810,12 +690,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
         p.ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + SK_COUNTER_BYTES);
         grid = static_cast<unsigned>(sk_grid(p.tiles, p.num_kb, sms));
     }
-    int cs = 0;
-    if constexpr (MT == 16) {
-        cs = xq ? sk_cluster_size<MT, true>(p.tiles, p.num_kb, sms) : sk_cluster_size<MT>(p.tiles, p.num_kb, sms);
-    } else {
-        cs = sk_cluster_size<MT>(p.tiles, p.num_kb, sms);
-    }
+    const int cs = sk_cluster_size<MT>(p.tiles, p.num_kb, sms);
     if (cs >= 2) {
         p.streamk = 2;
         p.cs = cs;
@@ -830,10 +705,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     // (Round 2 re-measured the full ring for every M <= 32 mode, and weight tiles issued two
     // k-blocks at a time: neither faster; the per-CTA stream is not bound by bytes in flight.)
     constexpr bool light = MT <= 32;
-    if constexpr (MT == 16)
-        cfg.dynamicSmemBytes = xq ? SkCfg<MT, light, true>::SMEM_BYTES : SkCfg<MT, light>::SMEM_BYTES;
-    else
-        cfg.dynamicSmemBytes = SkCfg<MT, light>::SMEM_BYTES;
+    cfg.dynamicSmemBytes = SkCfg<MT, light>::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     static const int no_pdl = [] {  // dev A/B: FP8Q_SKINNY_NOPDL=1 launches without PDL
@@ -848,11 +720,6 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if constexpr (MT == 16) {
-        if (xq) return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, light, true>, tmW, tmX, tmS, p);
-    } else {
-        if (xq) return cudaErrorInvalidValue;
-    }
     return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, light>, tmW, tmX, tmS, p);
 }
 
@@ -864,10 +731,6 @@ bool skinny_gemm_applies(const GemmArgs& a) {
         return e ? std::atoi(e) : 0;
     }();
     if (forced != 0 && forced != 16) return false;  // dev override: 16 = skinny, others = gemm.cu kinds
-    if (a.a_bf16 != nullptr) {  // fused activation quantization: decode kernel only, m <= 64
-        if (a.offsets != nullptr || a.m < 1 || a.m > kSkinnyMaxXQ) return false;
-        return forced == 16 || a.m <= 32 || (a.n + 255) / 256 < 64;
-    }
     if (a.offsets != nullptr || a.m < 1 || a.m > kSkinnyMaxM || (reinterpret_cast<uintptr_t>(a.sa) & 15u) != 0 ||
         (a.ld_sa % 4) != 0)
         return false;

@@ -68,13 +68,7 @@ struct GemmArgs {
     int32_t groups;
     void* workspace;         // split-K workspace (zero-filled before first use), may be null
     size_t workspace_bytes;
-    // fused activation quantization (decode kernel, m <= kSkinnyMaxXQ): BF16 activations
-    // instead of a / sa; the kernel quantizes them per token per 128 channels itself
-    const uint16_t* a_bf16 = nullptr;
-    int64_t ld_a_bf16 = 0;
-    int32_t* flag = nullptr;  // non-finite activation flag of the fused quantization
 };
-constexpr int kSkinnyMaxXQ = 8;
 
 // Decode-sized dense GEMMs (1 <= m <= kSkinnyMaxM) run the swap-AB kernel of gemm_skinny.cu
 // (m > 128 only where its cluster split-K mode applies).

@@ -427,7 +427,7 @@ def fp8_linear_dynamic(x: torch.Tensor, b: torch.Tensor, b_scales: torch.Tensor,
                        nonfinite_flag: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """One W8A8 linear with dynamic activation quantization: BF16 x [m,k],
     b codes [n,k], b_scales [ceil(n/128), >=k/128] -> D [m, n]; bit-identical to
-    quantize_act_per_token_group followed by fp8_block_gemm (decode sizes: one fused kernel)."""
+    quantize_act_per_token_group followed by fp8_block_gemm (two PDL-chained launches)."""
     _cuda2d(x, "x", torch.bfloat16)
     _cuda2d(b, "b", torch.uint8)
     _cuda2d(b_scales, "b_scales", torch.float32)

@@ -1,8 +1,8 @@
 """fp8_linear_dynamic: one W8A8 linear with the activations quantized
-dynamically inside the call -- at decode sizes by the decode GEMM kernel itself (fused, one
-launch).  Bar: BIT-identical to quantize_act_per_token_group followed by fp8_block_gemm (the
-same element map and GEMM), which the other suites pin to the oracle; plus a direct oracle
-check (codes/scales through the oracle quantizer, fp64 GEMM) on sampled outputs."""
+dynamically inside the call (the quantizer and the GEMM chained by programmatic dependent
+launch, the codes in the caller's workspace).  Bar: BIT-identical to the separate
+quantize_act_per_token_group + fp8_block_gemm calls (which the other suites pin to the oracle);
+plus a direct oracle check (oracle quantizer, fp64 GEMM) on the outputs."""
 import numpy as np
 import pytest
 import torch
