@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfp8q.so")
 SOURCES = ["capi.cu", "quant.cu", "gemm.cu", "gemm_skinny.cu", "producers.cu", "kv.cu", "mx.cu"]
-HEADERS = ["ptx.cuh", "quant_kernels.h", "scale_tables.cuh", "packed.cuh", "group_quant.cuh"]
+HEADERS = ["ptx.cuh", "quant_kernels.h", "scale_tables.cuh", "packed.cuh", "group_quant.cuh", "pdl.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -54,6 +54,7 @@ constexpr int SMEM_BUDGET = 160 * 1024;
 // Output staging for the TMA-store epilogue: per promotion warp four 32-row x 64-byte
 // chunks (2 KB each, 64-byte swizzle) -> 8 warps x 8 KB.  A BF16 half-tile row segment
 // (128 columns) is exactly 4 chunks, so a tile's stores never wait for each other.
+constexpr int kSmemGroups = 512;  // groups whose offsets the one-CTA kernel stages in smem
 constexpr int EPI_CHUNKS = 4;
 constexpr int EPI_CHUNK_BYTES = 32 * 64;
 constexpr int EPI_STAGE_BYTES = NUM_EPI_WARPS * EPI_CHUNKS * EPI_CHUNK_BYTES;
@@ -111,19 +112,21 @@ struct TileCursor {
     int row0;    // first A/D row of group g
     int rows;    // rows in group g
     int mtiles;  // ceil(rows / TM)
+    const int32_t* offs;  // the group offsets: a shared-memory copy when the kernel made one
     __device__ void load(const KParams& p) {
         if (p.offsets != nullptr) {
-            row0 = p.offsets[g];
-            rows = p.offsets[g + 1] - row0;
+            row0 = offs[g];
+            rows = offs[g + 1] - row0;
         } else {
             row0 = 0;
             rows = static_cast<int>(p.m);
         }
         mtiles = (rows + TM - 1) / TM;
     }
-    __device__ void init(const KParams& p) {
+    __device__ void init(const KParams& p, const int32_t* smem_offs = nullptr) {
         g = 0;
         base = 0;
+        offs = smem_offs != nullptr ? smem_offs : p.offsets;
         if (p.groups > 0) load(p);
     }
     // Returns false when t is past the last tile.
@@ -482,6 +485,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint64_t* stg_full = tempty + NBUF;   // [2]: per column half, 4 promotion warps arrive
     uint64_t* stg_empty = stg_full + 2;   // [2]: the store warp of that half arrives
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + 2);
+    // MoE: the group offsets in shared memory -- every role's tile cursor walks them at every
+    // tile, and from global memory each step of that walk is a dependent L2 round trip
+    __shared__ int32_t s_offs[kSmemGroups + 1];
+    const bool offs_smem = p.offsets != nullptr && p.groups <= kSmemGroups;
+    if (offs_smem)
+        for (int i = threadIdx.x; i <= p.groups; i += blockDim.x) s_offs[i] = p.offsets[i];
+    const int32_t* offs = offs_smem ? s_offs : nullptr;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -514,7 +524,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
             TileCursor<BM, RASTER_GM> cur;
-            cur.init(p);
+            cur.init(p, offs);
             uint32_t it = 0;
             int mt, nt;
             for (int item = blockIdx.x;; item += gridDim.x) {
@@ -538,7 +548,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // ------------------------------------------------------------ MMA issuer
             const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
             TileCursor<BM, RASTER_GM> cur;
-            cur.init(p);
+            cur.init(p, offs);
             uint32_t it = 0;
             int mt, nt;
             for (int item = blockIdx.x;; item += gridDim.x) {
@@ -569,7 +579,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ------------------------------------------------------------ store warps (BF16)
         const int h = warp - 2;
         TileCursor<BM, RASTER_GM> cur;
-        cur.init(p);
+        cur.init(p, offs);
         uint32_t tile_no = 0;
         int mt, nt;
         for (int t = blockIdx.x; cur.seek(p, t, mt, nt); t += gridDim.x) {
@@ -590,7 +600,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) tma_prefetch_desc(&tmD);
         const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
         TileCursor<BM, RASTER_GM> cur;
-        cur.init(p);
+        cur.init(p, offs);
         uint32_t it = 0;
         uint32_t tile_no = 0;
         auto make_tile = [&](int item, int mt, int nt) {

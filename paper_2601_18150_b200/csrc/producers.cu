@@ -27,6 +27,7 @@
 #include <mutex>
 
 #include "packed.cuh"
+#include "pdl.cuh"
 #include "ptx.cuh"
 #include "quant_kernels.h"
 #include "scale_tables.cuh"
@@ -219,8 +220,10 @@ __global__ void __launch_bounds__(256, 3) rmsnorm_quantize_kernel(
     constexpr int P1 = NV > 0 && NV < 8 ? NV : 8;  // pass-1 loads in flight per lane
     constexpr int U2 = NV > 0 && NV < 4 ? NV : 4;  // pass-2 vectors (x and gamma) loaded before use
     __shared__ ScaleTables tabs;
+    pdl_launch_dependents();
     init_scale_tables(tabs);
     __syncthreads();
+    pdl_wait();  // x is the previous kernel's output (pdl.cuh)
     const int lane = threadIdx.x & 31;
     const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
     for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); row < m; row += warps) {
@@ -357,6 +360,8 @@ __global__ void __launch_bounds__(SILU_THREADS, 1) silu_mul_quantize_kernel(
     int64_t chunks, int32_t* __restrict__ flag) {
     extern __shared__ __align__(16) uint16_t stab[];
     __shared__ ScaleTables tabs;
+    pdl_launch_dependents();
+    pdl_wait();  // gate_up (and, on a first call, the table build) come from preceding kernels
     {
         const uint4* src = reinterpret_cast<const uint4*>(g_silu_tab);
         uint4* dst = reinterpret_cast<uint4*>(stab);
@@ -427,19 +432,17 @@ cudaError_t launch_rmsnorm_quantize(const uint16_t* x, const uint16_t* gamma, fl
     const unsigned grid = static_cast<unsigned>(rows_blocks < cap ? rows_blocks : cap);
     if (k % 256 == 0 && k <= 4096) {
         switch (k / 256) {
-#define RMS_FIXED(NV)                                                                                        \
-    case NV:                                                                                                 \
-        rmsnorm_quantize_kernel<NV><<<grid, 256, 0, stream>>>(x, gamma, eps, m, k, ld_x, q, ld_q, scales, ld_s, \
-                                                              y, ld_y, flag);                                 \
-        return cudaGetLastError();
+#define RMS_FIXED(NV)                                                                                   \
+    case NV:                                                                                            \
+        return launch_pdl(rmsnorm_quantize_kernel<NV>, grid, 256, 0, stream, x, gamma, eps, m, k, ld_x, q, \
+                          ld_q, scales, ld_s, y, ld_y, flag);
             RMS_FIXED(1) RMS_FIXED(2) RMS_FIXED(4) RMS_FIXED(8) RMS_FIXED(12) RMS_FIXED(16)
 #undef RMS_FIXED
             default: break;
         }
     }
-    rmsnorm_quantize_kernel<0><<<grid, 256, 0, stream>>>(x, gamma, eps, m, k, ld_x, q, ld_q, scales, ld_s, y, ld_y,
-                                                         flag);
-    return cudaGetLastError();
+    return launch_pdl(rmsnorm_quantize_kernel<0>, grid, 256, 0, stream, x, gamma, eps, m, k, ld_x, q, ld_q, scales,
+                      ld_s, y, ld_y, flag);
 }
 
 namespace {
@@ -514,12 +517,11 @@ cudaError_t launch_silu_mul_quantize(const uint16_t* gu, int64_t m, int64_t inte
     int64_t grid = (items + per_cta - 1) / per_cta;
     grid = grid < sms() ? grid : sms();
     if ((inter / 128) % 8 == 0)
-        silu_mul_quantize_kernel<true><<<static_cast<unsigned>(grid), SILU_THREADS, SILU_SMEM, stream>>>(
-            gu, m, inter, ld_gu, q, ld_q, scales, ld_s, y, ld_y, chunks, flag);
+        return launch_pdl(silu_mul_quantize_kernel<true>, static_cast<unsigned>(grid), SILU_THREADS, SILU_SMEM, stream,
+                          gu, m, inter, ld_gu, q, ld_q, scales, ld_s, y, ld_y, chunks, flag);
     else
-        silu_mul_quantize_kernel<false><<<static_cast<unsigned>(grid), SILU_THREADS, SILU_SMEM, stream>>>(
-            gu, m, inter, ld_gu, q, ld_q, scales, ld_s, y, ld_y, chunks, flag);
-    return cudaGetLastError();
+        return launch_pdl(silu_mul_quantize_kernel<false>, static_cast<unsigned>(grid), SILU_THREADS, SILU_SMEM,
+                          stream, gu, m, inter, ld_gu, q, ld_q, scales, ld_s, y, ld_y, chunks, flag);
 }
 
 }  // namespace fp8q

@@ -29,33 +29,12 @@
 #include "packed.cuh"
 #include "scale_tables.cuh"
 #include "group_quant.cuh"
+#include "pdl.cuh"
 
 namespace fp8q {
 
 namespace {
 
-// Programmatic dependent launch (the activation quantizers run between a GEMM producing their
-// input and the GEMM consuming their output): trigger the dependent launch early, and wait for
-// the preceding grid (complete + its memory visible) before touching x, codes or scales.
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-// Launch with the programmatic-stream-serialization attribute (PDL).
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
-                       Args&&... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
-}
 
 // RN32(x / s) for blocks with amax >= 2^-104 (see header comment), sign taken from x.
 __device__ __forceinline__ float quot_fast(float x, float s, float r) {
