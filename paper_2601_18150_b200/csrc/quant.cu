@@ -391,6 +391,60 @@ __device__ __forceinline__ void aq_process(const AItemRegs& d, uint8_t* __restri
         st_v4_na(q + row * ld_q + g * 128 + (lane & 7) * 16, c);
     }
 }
+// The staged kernel's encode of one item (same arithmetic as aq_process): 32-bit indices, the
+// item's row already resolved by the producer, and no divergent branches in the common case --
+// when every live group of the warp is on the fast path the encode is warp-uniform; the scale
+// and code stores are predicated instructions.
+__device__ __forceinline__ void st_global_f32_if(bool p, float* a, float v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.global.f32 [%1], %2;\n\t}" ::"r"(
+                     static_cast<uint32_t>(p)),
+                 "l"(a), "f"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void st_global_v4_na_if(bool p, void* a, const uint4& v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t"
+        "@q st.global.L1::no_allocate.v4.u32 [%1], {%2, %3, %4, %5};\n\t}" ::"r"(static_cast<uint32_t>(p)),
+        "l"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+        : "memory");
+}
+__device__ __forceinline__ void aq_process_item(const AItemRegs& d, uint8_t* __restrict__ qrow,
+                                                float* __restrict__ srow, uint32_t ld_s, uint32_t groups,
+                                                uint32_t chunk, int32_t* __restrict__ nonfinite_flag,
+                                                const ScaleTables& tabs) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t ab[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ab[j] = abs_max_bits16(d.v[j]);
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ab[j] = max(ab[j], __shfl_xor_sync(0xFFFFFFFFu, ab[j], off));
+    }
+    uint32_t bad = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t g = chunk * 16u + 4u * j + (lane >> 3);
+        const bool live = g < groups;
+        const bool fast = ab[j] >= kAmaxFastGuardBits && ab[j] < kNonFiniteBits;
+        float s, r = 0.0f;
+        uint4 c;
+        if (__all_sync(0xFFFFFFFFu, fast || !live)) {  // warp-uniform: the common case
+            table_scale_rcp(tabs, ab[j], s, r);
+            c = encode16<true>(d.v[j], s, r);
+        } else {
+            if (fast)
+                table_scale_rcp(tabs, ab[j], s, r);
+            else
+                s = scale_from_amax_bits(ab[j]);
+            c = fast ? encode16<true>(d.v[j], s, r) : encode16<false>(d.v[j], s, 0.0f);
+        }
+        st_global_f32_if(live && (lane & 7) == 0, srow + static_cast<uint64_t>(g) * ld_s, s);
+        bad |= (live && ab[j] >= kNonFiniteBits) ? 1u : 0u;
+        st_global_v4_na_if(live, qrow + g * 128 + (lane & 7) * 16, c);
+    }
+    if (bad && nonfinite_flag != nullptr) *nonfinite_flag = 1;
+}
 __global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
     const uint16_t* __restrict__ x, int64_t ld_x, uint8_t* __restrict__ q, int64_t ld_q,
     float* __restrict__ scales, int64_t ld_s, int64_t groups, int64_t chunks, int64_t items,
@@ -486,6 +540,9 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
     pdl_launch_dependents();
     uint64_t* full = reinterpret_cast<uint64_t*>(abq_smem + size_t(ABQ_STAGES) * ABQ_ITEMS * ABQ_ITEM_BYTES);
     uint64_t* empty = full + ABQ_STAGES;
+    // per item slot: {row, tensor << 16 | chunk}, written by the producer with the copy, so
+    // consumers need no division or tensor search per item
+    __shared__ uint2 meta[ABQ_STAGES * ABQ_ITEMS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // this CTA's equal share of the batch's items
     const int64_t i0 = ab.items * blockIdx.x / gridDim.x;
@@ -522,6 +579,8 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
                 uint32_t bytes = 0;
                 for (int j = 0; j < cnt; ++j) {
                     const ATensor& t = ab.t[ti];
+                    meta[s * ABQ_ITEMS + j] = make_uint2(static_cast<uint32_t>(row),
+                                                         (static_cast<uint32_t>(ti) << 16) | static_cast<uint32_t>(chunk));
                     // copies may complete before the expect_tx below: the phase cannot, since
                     // its one arrival (the expect_tx arrive) is still pending
                     if (kTma) {
@@ -560,16 +619,16 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
         mbar_wait(&full[s], static_cast<uint32_t>((it / ABQ_STAGES) & 1));
         const int64_t item = i0 + it * ABQ_ITEMS + w;
         if (item < i1) {
-            const ATensor& t = ab.t[tensor_of(item)];
-            // 32-bit (the host keeps each tensor's items < 2^31): once per 4 KB item
-            const uint32_t local = static_cast<uint32_t>(item - t.item0);
-            const int64_t row = local / static_cast<uint32_t>(t.chunks);
-            const int64_t chunk = local - row * t.chunks;
+            const uint2 md = meta[s * ABQ_ITEMS + w];
+            const ATensor& t = ab.t[md.y >> 16];
+            const uint32_t chunk = md.y & 0xFFFFu;
+            const uint32_t groups = static_cast<uint32_t>(t.groups);
             AItemRegs d;
-            aq_load_smem(ring + (s * ABQ_ITEMS + w) * ABQ_ITEM_BYTES, t.groups, chunk, d);
+            aq_load_smem(ring + (s * ABQ_ITEMS + w) * ABQ_ITEM_BYTES, groups, chunk, d);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // the item is in registers: free the slot
-            aq_process(d, t.q, t.ld_q, t.scales, t.ld_s, t.groups, row, chunk, nonfinite_flag, tabs);
+            aq_process_item(d, t.q + int64_t(md.x) * t.ld_q, t.scales + md.x, static_cast<uint32_t>(t.ld_s), groups,
+                            chunk, nonfinite_flag, tabs);
         } else {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
