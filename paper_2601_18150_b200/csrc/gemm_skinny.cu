@@ -622,9 +622,6 @@ int sk_cluster_size(int tiles, int num_kb, int sms) {
         q.numAttrs = 1;
         int active = 0;
         const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, fp8_gemm_skinny_kernel<MT, false>, &q);
-        if (std::getenv("FP8Q_DEBUG_CLUSTER") != nullptr)
-            std::fprintf(stderr, "[fp8q] skinny MT=%d tiles=%d kb=%d: cluster %d -> %d active (%s)\n", MT, tiles,
-                         num_kb, c, active, cudaGetErrorString(e));
         if (e == cudaSuccess && active >= tiles) break;
         cudaGetLastError();
     }

@@ -285,6 +285,41 @@ def test_act_batched_matches_oracle(shapes):
         assert np.array_equal(act_scales_logical(scales, m).view(np.uint32), os_.view(np.uint32)), (m, k)
 
 
+
+_ACT_SCRIPT = r"""
+import numpy as np, torch, oracle, synth
+from paper_2601_18150_b200 import fp8q
+from tests.helpers import to_dev_bf16, to_host_u8, act_scales_logical
+shapes = [(300, 4096), (257, 384), (1000, 2176), (513, 12288), (40, 1024), (1, 128)]
+items, ref = [], []
+for i, (m, k) in enumerate(shapes):
+    bits = synth.qwen3_activation(m, k, seed=800 + i)
+    items.append((to_dev_bf16(bits), torch.full((m, k), 0xAB, dtype=torch.uint8, device="cuda"),
+                  torch.full((k // 128, fp8q.act_scales_ld(m)), -1.0, dtype=torch.float32, device="cuda")))
+    ref.append(oracle.quantize_act_per_token_group(bits))
+fp8q.quantize_act_per_token_group_batched(items)
+torch.cuda.synchronize()
+for (m, k), (x, codes, scales), (oc, os_) in zip(shapes, items, ref):
+    assert np.array_equal(to_host_u8(codes), oc), (m, k)
+    assert np.array_equal(act_scales_logical(scales, m).view(np.uint32), os_.view(np.uint32)), (m, k)
+print("act ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"FP8Q_ACT_KERNEL": "wide"}, {"FP8Q_ACT_LOAD": "bulk"}])
+def test_act_forced_path_ragged(env):
+    # The dev switches pick another activation kernel (warp-persistent register kernel for
+    # every size) or another load form (cp.async.bulk rows instead of TMA boxes); the bytes must
+    # not change.  Fresh process: the switches are read once.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _ACT_SCRIPT], cwd=root, env=dict(os.environ, PYTHONPATH=root, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "act ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_act_batched_equals_single_calls_full_size():
     # the bench step's inputs: [8192, 4096] x 3 + [8192, 12288] in one launch == four launches
     g = torch.Generator(device="cuda")
