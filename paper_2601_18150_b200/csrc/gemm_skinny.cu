@@ -20,6 +20,14 @@
 // per-CTA timeline showed the stream-K fixup (fence, counter atomics, one dependent L2 round
 // trip per contributor, 64 KB of partials per contributor at M = 128) ending 5-12 us after the
 // last weight byte arrived; the DSMEM reduction replaces it with two cluster barriers.
+// When every range spans at least one tile's k-blocks (>= 148 tiles, e.g. gate_up), a tile has
+// at most two CTAs and the stream-K runs ORDERED: each CTA does the head of its last tile first
+// (parked + flagged), then its whole tiles, then the tail of its first tile, which it combines
+// with the long-published head -- no atomics, and no fixup round trips after the stream.
+// One CTA per SM (the full ring at every M): with two per SM, programmatic dependent launch let
+// the block scheduler put two CTAs of the SAME grid on one SM (up to 34 of 148 at M = 1), and
+// those streamed their ranges 3-4 us late.  The dependants are released after the producer's
+// last TMA issue (the tail), not at entry.
 //
 // CTA = 12 warps (3 warpgroups):
 //   warp 0       TMA producer: per k-block W 128x128 B, X MTx128 B (rows >= m zero-filled by
@@ -43,12 +51,12 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
 #include "ptx.cuh"
 #include "quant_kernels.h"
+#include "trace.cuh"
 
 namespace fp8q {
 namespace {
@@ -72,7 +80,7 @@ constexpr int pow2_at_least(int v, int lo) {
     return p;
 }
 
-template <int MT, bool L = (MT <= 32)>
+template <int MT>
 struct SkCfg {
     static constexpr int W_TILE = SK_BN * SK_BK;   // 16 KB
     static constexpr int X_TILE = MT * SK_BK;      // MT x 128 B (a multiple of 1024 B: SW128 atoms)
@@ -80,12 +88,7 @@ struct SkCfg {
     static constexpr int SA_SLOT = SA_BYTES < 128 ? 128 : SA_BYTES;  // TMA smem dst: 128-B aligned
     static constexpr int STAGE_BYTES = W_TILE + X_TILE;
     static constexpr int TX_BYTES = STAGE_BYTES + SA_BYTES;  // TMA bytes per stage
-    // MT <= 32: half the smem, registers and TMEM, so two CTAs -- this GEMM's and the next
-    // one's (programmatic dependent launch) -- fit on an SM and the next GEMM's weight stream
-    // starts while this one drains
-    static constexpr bool LIGHT = L;
-    static constexpr int BUDGET = LIGHT ? SK_SMEM_BUDGET / 2 : SK_SMEM_BUDGET;
-    static constexpr int STAGES_RAW = BUDGET / (STAGE_BYTES + SA_SLOT);
+    static constexpr int STAGES_RAW = SK_SMEM_BUDGET / (STAGE_BYTES + SA_SLOT);
     static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
     static constexpr int NBUF_RAW = 512 / MT;
     static constexpr int NBUF = NBUF_RAW > 8 ? 8 : NBUF_RAW;  // TMEM partial buffers
@@ -108,7 +111,10 @@ struct SkParams {
     int m, n, num_kb, tiles;
     int streamk;        // 1: ranges [c*T/G, (c+1)*T/G) per CTA; 0: whole tiles, strided;
                         // 2: cluster split-K -- cluster = one tile, CTA rank r its k-blocks
-                        //    [r*KB/cs, (r+1)*KB/cs), partials reduced through DSMEM
+                        //    [r*KB/cs, (r+1)*KB/cs), partials reduced through DSMEM;
+                        // 3: ordered stream-K (ranges >= KB, so a tile has <= 2 CTAs): the
+                        //    range's last, partial tile first (parked + flagged), whole tiles,
+                        //    then its first, partial tile, combined with the parked head
     int cs;             // cluster size (mode 2)
     int64_t total;      // T = tiles * num_kb
     float* ws;          // stream-K partials: two [MT][128] fp32 slots per CTA
@@ -117,17 +123,53 @@ struct SkParams {
 __device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Walks this CTA's segments: (tile, kb0, kb1) = k-blocks [kb0, kb1) of weight tile `tile`.
-struct SegIter {
+template <bool kOrdered>  // false: the ordered stream-K branch compiled out (MT = 256, cluster mode only)
+struct SegIterT {
     int64_t x, end;  // stream-K: position in [0, T) and this CTA's range end
-    int t;           // tiled: next tile
+    int t;           // tiled: next tile (ordered stream-K: next whole tile)
+    int phase;       // ordered stream-K: 0 head of the last tile, 1 whole tiles, 2 tail of the first, 3 done
     __device__ __forceinline__ void init(const SkParams& p) {
-        if (p.streamk == 1) {
+        if (p.streamk == 1 || p.streamk == 3) {
             x = static_cast<int64_t>(blockIdx.x) * p.total / gridDim.x;
             end = static_cast<int64_t>(blockIdx.x + 1) * p.total / gridDim.x;
         }
         t = blockIdx.x;
+        if (kOrdered && p.streamk == 3) {
+            t = static_cast<int>((x + p.num_kb - 1) / p.num_kb);  // first whole tile
+            phase = 0;
+        }
     }
     __device__ __forceinline__ bool next(const SkParams& p, int& tile, int& kb0, int& kb1) {
+        if (kOrdered && p.streamk == 3) {
+            if (phase == 0) {
+                phase = 1;
+                if (end % p.num_kb != 0) {  // head of the range's last tile (shared with the next CTA)
+                    tile = static_cast<int>(end / p.num_kb);
+                    kb0 = 0;
+                    kb1 = static_cast<int>(end % p.num_kb);
+                    return true;
+                }
+            }
+            if (phase == 1) {
+                if (t < static_cast<int>(end / p.num_kb)) {
+                    tile = t++;
+                    kb0 = 0;
+                    kb1 = p.num_kb;
+                    return true;
+                }
+                phase = 2;
+            }
+            if (phase == 2) {
+                phase = 3;
+                if (x % p.num_kb != 0) {  // tail of the range's first tile (shared with the previous CTA)
+                    tile = static_cast<int>(x / p.num_kb);
+                    kb0 = static_cast<int>(x % p.num_kb);
+                    kb1 = p.num_kb;
+                    return true;
+                }
+            }
+            return false;
+        }
         if (p.streamk == 2) {  // one segment: rank r of cluster `tile`
             if (t < 0) return false;
             const int r = static_cast<int>(blockIdx.x) % p.cs;
@@ -198,11 +240,12 @@ __device__ __forceinline__ void sk_store(const SkParams& p, int64_t n_row, int j
     }
 }
 
-template <int MT, bool L>
-__global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
+template <int MT>
+__global__ void __launch_bounds__(SK_THREADS, 1)
     fp8_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                            const __grid_constant__ CUtensorMap tmS, const SkParams p) {
-    using C = SkCfg<MT, L>;
+    using C = SkCfg<MT>;
+    using SegIter = SegIterT<(MT <= 128)>;
     constexpr int STAGES = C::STAGES;
     constexpr int NBUF = C::NBUF;
     constexpr int COLS = C::COLS;
@@ -222,6 +265,9 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t trace_tag = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p.sb));
+    (void)trace_tag;
+    if (threadIdx.x == 0) FP8Q_TREC(trace_tag, 0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -238,10 +284,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    // let the next kernel in the stream (launched with programmatic stream serialization)
-    // start its prologue and weight prefetch on SMs this grid vacates
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (!C::LIGHT && warp < SK_EPI_WARP0) regs_dec<SK_REGS_CTRL>();
+    if (warp < SK_EPI_WARP0) regs_dec<SK_REGS_CTRL>();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -268,6 +311,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                     }
             }
             grid_dependency_wait();
+            FP8Q_TREC(trace_tag, 1);
             while (seg.next(p, tile, kb0, kb1)) {
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
@@ -285,6 +329,10 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                     tma_load_2d(smS + stage * SA_STRIDE, &tmS, &full[stage], 0, kb);
                 }
             }
+            FP8Q_TREC(trace_tag, 2);
+            // every weight byte is requested: let the next kernel in the stream (programmatic
+            // stream serialization) launch and start its prologue / weight prefetch in our tail
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -302,6 +350,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                     const uint32_t bph = (it / NBUF) & 1u;
                     mbar_wait(&tempty[buf], bph ^ 1u);
                     mbar_wait(&full[stage], ph);
+                    if (it == 0) FP8Q_TREC(trace_tag, 3);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(smW + stage * C::W_TILE);
                     const uint32_t b0 = smem_u32(smX + stage * C::X_TILE);
@@ -314,11 +363,13 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                     mma_commit(&tfull[buf]);
                 }
             }
+            FP8Q_TREC(trace_tag, 4);
         }
     } else if (warp >= SK_EPI_WARP0) {
         // ---------------------------------------------------------------- promotion warps
-        if (!C::LIGHT) regs_inc<SK_REGS_EPI>();
+        regs_inc<SK_REGS_EPI>();
         grid_dependency_wait();  // before any global write (D, workspace): the previous grid is done
+        if (threadIdx.x == SK_EPI_WARP0 * 32) FP8Q_TREC(trace_tag, 5);
         const int qd = warp & 3;                       // TMEM lane quarter of this warp
         const int h = (warp - SK_EPI_WARP0) >> 2;      // token-column half
         const int r_in = qd * 32 + lane;               // weight row within the tile
@@ -380,6 +431,39 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                 float* red = reinterpret_cast<float*>(smW) + j0 * SK_BN + r_in;
 #pragma unroll
                 for (int j = 0; j < COLS; ++j) red[j * SK_BN] = acc[j];
+            } else if (MT <= 128 && p.streamk == 3 && kb1 < p.num_kb) {  // (M > 128: cluster mode only)
+                // ordered stream-K, head of a shared tile (this CTA's first segment): park it in
+                // slot 0 and flag it; the next CTA, which holds the tile's tail as its LAST
+                // segment, will find it long published
+                float* mine = p.ws + (int64_t(2 * blockIdx.x) * MT + j0) * SK_BN + r_in;
+#pragma unroll
+                for (int j = 0; j < COLS; ++j)
+                    if (j < jn) mine[j * SK_BN] = acc[j];
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"n"(SK_EPI_WARPS * 32) : "memory");
+                if (threadIdx.x == SK_EPI_WARP0 * 32)
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.counters + tile), "r"(1) : "memory");
+            } else if (MT <= 128 && p.streamk == 3 && kb0 > 0) {
+                // ordered stream-K, tail of a shared tile (this CTA's last segment): head + tail
+                // in CTA order, (0 + P_head) + P_tail as the atomic fixup sums it
+                if (threadIdx.x == SK_EPI_WARP0 * 32) {
+                    int f = 0;
+                    for (;;) {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.counters + tile) : "memory");
+                        if (f != 0) break;
+                        __nanosleep(64);
+                    }
+                    p.counters[tile] = 0;  // reusable workspace
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(SK_EPI_WARPS * 32) : "memory");
+                const int c_head = sk_cta_of(p, int64_t(tile) * p.num_kb);
+                const float* src = p.ws + (int64_t(2 * c_head) * MT + j0) * SK_BN + r_in;
+                float v[COLS];
+#pragma unroll
+                for (int j = 0; j < COLS; ++j) v[j] = __ldcg(src + j * SK_BN);
+#pragma unroll
+                for (int j = 0; j < COLS; ++j) acc[j] = (0.0f + v[j]) + acc[j];
+                if (n_row < p.n) sk_store(p, n_row, j0, jn, acc);
             } else if (kb0 > 0 || kb1 < p.num_kb) {
                 // partial tile (first or last segment of this CTA's range): park it, no wait
                 const int slot = si == 0 ? 0 : 1;
@@ -394,6 +478,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                 sk_store(p, n_row, j0, jn, acc);
             }
         }
+        if (threadIdx.x == SK_EPI_WARP0 * 32) FP8Q_TREC(trace_tag, 6);
         // ---- stream-K fixup of the parked tiles (at most two per CTA): one fence, both
         // counters bumped in one round trip, then the sums of the tiles this CTA completes
         if (parked[0] >= 0 || parked[1] >= 0) {
@@ -429,7 +514,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
                 // the per-CTA timeline showed the fixup CTAs exiting ~8 us after their stream
                 // ended with one dependent round trip per contributor) and summed in CTA order,
                 // so the result is bit-identical to the one-at-a-time sum.
-                constexpr int FC_REGS = C::LIGHT ? 32 : 64;  // light: 80 registers per thread in all
+                constexpr int FC_REGS = 64;
                 constexpr int FC = COLS >= FC_REGS ? 1 : FC_REGS / COLS;
                 float acc[COLS];
 #pragma unroll
@@ -533,6 +618,7 @@ __global__ void __launch_bounds__(SK_THREADS, L ? 2 : 1)
         tc_fence_after();
         tmem_dealloc(*reinterpret_cast<volatile uint32_t*>(tmem_slot), C::TMEM_COLS);
     }
+    if (threadIdx.x == SK_EPI_WARP0 * 32) FP8Q_TREC(trace_tag, 7);
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -571,17 +657,15 @@ cudaError_t sk_device_info(int& sms) {
     if (!di.attr_set) {
         e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return e;
-#define SK_ATTR(MT, L)                                                                                  \
-    e = cudaFuncSetAttribute(fp8_gemm_skinny_kernel<MT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             static_cast<int>(SkCfg<MT, L>::SMEM_BYTES));                                \
+#define SK_ATTR(MT)                                                                                  \
+    e = cudaFuncSetAttribute(fp8_gemm_skinny_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             static_cast<int>(SkCfg<MT>::SMEM_BYTES));                                \
     if (e != cudaSuccess) return e;
-        SK_ATTR(16, true)
-        SK_ATTR(16, false)
-        SK_ATTR(32, true)
-        SK_ATTR(32, false)
-        SK_ATTR(64, false)
-        SK_ATTR(128, false)
-        SK_ATTR(256, false)
+        SK_ATTR(16)
+        SK_ATTR(32)
+        SK_ATTR(64)
+        SK_ATTR(128)
+        SK_ATTR(256)
 #undef SK_ATTR
         di.attr_set = true;
     }
@@ -612,7 +696,7 @@ int sk_cluster_size(int tiles, int num_kb, int sms) {
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3(static_cast<unsigned>(tiles * c));
         q.blockDim = dim3(SK_THREADS);
-        q.dynamicSmemBytes = SkCfg<MT, false>::SMEM_BYTES;
+        q.dynamicSmemBytes = SkCfg<MT>::SMEM_BYTES;
         cudaLaunchAttribute ca;
         ca.id = cudaLaunchAttributeClusterDimension;
         ca.val.clusterDim.x = static_cast<unsigned>(c);
@@ -621,7 +705,7 @@ int sk_cluster_size(int tiles, int num_kb, int sms) {
         q.attrs = &ca;
         q.numAttrs = 1;
         int active = 0;
-        const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, fp8_gemm_skinny_kernel<MT, false>, &q);
+        const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, fp8_gemm_skinny_kernel<MT>, &q);
         if (e == cudaSuccess && active >= tiles) break;
         cudaGetLastError();
     }
@@ -686,6 +770,13 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
         p.counters = static_cast<int32_t*>(a.workspace);
         p.ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + SK_COUNTER_BYTES);
         grid = static_cast<unsigned>(sk_grid(p.tiles, p.num_kb, sms));
+        static const bool ordered = [] {  // dev A/B: FP8Q_SKINNY_ORDERED=0 keeps the atomic fixup
+            const char* e = std::getenv("FP8Q_SKINNY_ORDERED");
+            return !(e != nullptr && e[0] == '0');
+        }();
+        // every range spans >= one tile's k-blocks, so each tile has at most two CTAs: the
+        // ordered form (no atomics, the shared heads published at the start)
+        if (ordered && p.total / grid >= p.num_kb) p.streamk = 3;
     }
     const int cs = sk_cluster_size<MT>(p.tiles, p.num_kb, sms);
     if (cs >= 2) {
@@ -696,13 +787,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(SK_THREADS);
-    // M <= 32: the half-budget config (two CTAs per SM, so the next GEMM's CTAs start under
-    // PDL while this one drains), in every mode.  (Round 1 measured the full ring in cluster
-    // mode: qkv 11.6 -> 10.9 us but o_proj 7.9 -> 8.5 us per GEMM at M = 1; not adopted.)
-    // (Round 2 re-measured the full ring for every M <= 32 mode, and weight tiles issued two
-    // k-blocks at a time: neither faster; the per-CTA stream is not bound by bytes in flight.)
-    constexpr bool light = MT <= 32;
-    cfg.dynamicSmemBytes = SkCfg<MT, light>::SMEM_BYTES;
+    cfg.dynamicSmemBytes = SkCfg<MT>::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     static const int no_pdl = [] {  // dev A/B: FP8Q_SKINNY_NOPDL=1 launches without PDL
@@ -717,7 +802,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT, light>, tmW, tmX, tmS, p);
+    return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT>, tmW, tmX, tmS, p);
 }
 
 }  // namespace
@@ -765,3 +850,5 @@ cudaError_t launch_fp8_gemm_skinny(const GemmArgs& a, void* encode_fn, cudaStrea
 }
 
 }  // namespace fp8q
+
+FP8Q_TRACE_DUMP_FN(fp8q_trace_dump_skinny)

@@ -30,6 +30,7 @@
 #include "scale_tables.cuh"
 #include "group_quant.cuh"
 #include "pdl.cuh"
+#include "trace.cuh"
 
 namespace fp8q {
 
@@ -450,10 +451,14 @@ __global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
     float* __restrict__ scales, int64_t ld_s, int64_t groups, int64_t chunks, int64_t items,
     int32_t* __restrict__ nonfinite_flag) {
     __shared__ ScaleTables tabs;
+    const uint32_t trace_tag = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(x));
+    (void)trace_tag;
+    if (threadIdx.x == 0) FP8Q_TREC(trace_tag, 10);
     pdl_launch_dependents();  // the consumer GEMM may start its weight prefetch now
     init_scale_tables(tabs);
     __syncthreads();
     pdl_wait();  // x is the previous kernel's output; q / scales may still be read by it
+    if (threadIdx.x == 0) FP8Q_TREC(trace_tag, 11);
     const int64_t warps = static_cast<int64_t>(gridDim.x) * 8;
     int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     AItemRegs a, b;
@@ -469,6 +474,7 @@ __global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
         aq_process(b, q, ld_q, scales, ld_s, groups, item / chunks, item % chunks, nonfinite_flag, tabs);
         item = nxt;
     }
+    if (threadIdx.x == 0) FP8Q_TREC(trace_tag, 12);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1066,3 +1072,5 @@ cudaError_t launch_act_per_token_group(const uint16_t* x, int64_t m, int64_t k, 
 }
 
 }  // namespace fp8q
+
+FP8Q_TRACE_DUMP_FN(fp8q_trace_dump_quant)

@@ -241,6 +241,9 @@ def test_splitk_workspace_reused_across_shapes():
     (5, 128 * 21, 2048), (40, 128 * 29 + 64, 1024), (2, 128 * 37, 4096), (9, 128 * 74, 512),
     # M = 129..256: the swap-AB kernel with 256 token columns, cluster split-K only
     (200, 4096, 4096), (256, 1000, 2048), (129, 6144, 1024),
+    # >= 148 weight tiles: ordered stream-K (every range >= one tile of k-blocks; gate_up at M = 1,
+    # a ragged last tile, 4-k-block tiles) and, with ranges < one tile, the atomic fixup
+    (1, 24576, 4096), (7, 128 * 150 + 40, 1024), (20, 128 * 300, 512), (1, 128 * 100, 4096),
 ])
 def test_skinny_decode_vs_oracle(m, n, k):
     # 1 <= m <= 128 (dense) runs gemm_skinny.cu: tokens in the MMA N dimension (16..128 padded
@@ -310,6 +313,35 @@ def test_skinny_streamk_path_when_cluster_split_disabled():
     r = subprocess.run([sys.executable, "-c", _STREAMK_SCRIPT], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "streamk ok" in r.stdout, r.stdout + r.stderr
+
+
+_ORDERED_SCRIPT = r"""
+import hashlib, sys, torch
+from tests.test_gpu_gemm import _operands, _run
+h = hashlib.sha256()
+for i, (m, n, k) in enumerate([(1, 24576, 4096), (16, 24576, 4096), (32, 128 * 151 + 8, 2048), (5, 128 * 300, 512)]):
+    a, sa, b, sb = _operands(m, n, k, 120 + i)
+    h.update(_run(a, sa, b, sb).cpu().numpy().tobytes())
+print("digest", h.hexdigest())
+"""
+
+
+def test_skinny_ordered_streamk_equals_atomic_fixup():
+    # The ordered stream-K form (shared heads parked and flagged first, the owner combining them
+    # last) adds the same two partials in the same order as the atomic last-arriver fixup: the
+    # outputs are bitwise identical (FP8Q_SKINNY_ORDERED=0 forces the atomic form; fresh processes).
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = []
+    for flag in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", _ORDERED_SCRIPT], cwd=root,
+                           env=dict(os.environ, FP8Q_SKINNY_ORDERED=flag, PYTHONPATH=root),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "digest" in r.stdout, r.stdout + r.stderr
+        out.append(r.stdout.split("digest")[1].strip())
+    assert out[0] == out[1]
 
 
 _KIND_SCRIPT = r"""
