@@ -95,7 +95,7 @@ struct KParams {
     int num_n_tiles;
     const int32_t* offsets;  // nullptr: one group of m rows
     int splits;              // split-K slices per tile (one-CTA kernel, dense, small M); 1 = off
-    int raster;              // m-tiles per raster band (TileCursor)
+    int raster;              // m-tiles per raster band (TileCursor); < 0: -(n-tiles per band), n fastest
     float* ws;               // split-K partials [tile][split][128][BN] fp32
     int32_t* counters;       // split-K arrival counters [tile], zero between launches
     int groups;
@@ -140,8 +140,20 @@ struct TileCursor {
         // Grouped raster: bands of GM m-tiles; inside a band m is fastest, so the ~148
         // concurrent tiles cover a compact RASTER_GM x ~9 block of the output and both the A
         // band and the B tiles they touch stay L2-resident (K = 12288 would otherwise re-read A).
-        const unsigned GM = static_cast<unsigned>(p.raster);
         const unsigned l = static_cast<unsigned>(t - base);
+        if (p.raster < 0) {  // B-resident raster: bands of -raster n-tiles, n fastest inside
+            const unsigned GN = static_cast<unsigned>(-p.raster);
+            const unsigned nt_all = static_cast<unsigned>(p.num_n_tiles);
+            const unsigned spn = GN * static_cast<unsigned>(mtiles);
+            const unsigned bn = l / spn;
+            const unsigned rn = l - bn * spn;
+            const unsigned gn = min(GN, nt_all - bn * GN);
+            const unsigned qn = rn / gn;
+            nt = static_cast<int>(bn * GN + (rn - qn * gn));
+            mt = static_cast<int>(qn);
+            return true;
+        }
+        const unsigned GM = static_cast<unsigned>(p.raster);
         const unsigned span = GM * static_cast<unsigned>(p.num_n_tiles);
         const unsigned band = l / span;
         const unsigned r = l - band * span;
@@ -1008,7 +1020,18 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
         r = r < 4 ? 4 : (r > 64 ? 64 : r);
         // measured (FP8Q_GEMM_RASTER sweep, pair kernel): gate_up (K = 4096) +1.5 % at 32
         // m-tiles per band vs 8; down (K = 12288) best at 8-16; qkv / o insensitive
-        p.raster = forced_raster > 0 ? forced_raster : (kPair ? static_cast<int>(r) : RASTER_GM);
+        p.raster = forced_raster != 0 ? forced_raster : (kPair ? static_cast<int>(r) : RASTER_GM);
+        // B smaller than A and all of it fits in ~64 MB of L2 (down_proj: B 50 MB vs A 100 MB):
+        // keep B resident instead -- bands of n-tiles covering all of N, n fastest, so A streams
+        // from HBM once and B once (the m-band raster re-reads B once per band: 2.8x the operand
+        // bytes for down_proj)
+        static const bool b_resident = [] {  // dev A/B: FP8Q_GEMM_BRES=0 keeps the m-band raster
+            const char* e = std::getenv("FP8Q_GEMM_BRES");
+            return !(e != nullptr && e[0] == '0');
+        }();
+        if (forced_raster == 0 && kPair && b_resident && a.offsets == nullptr && a.n < a.m &&
+            a.n * a.k <= (64LL << 20))
+            p.raster = -p.num_n_tiles;
     }
     if (!kPair && KIND == 256 && a.offsets == nullptr) {
         const int sp = plan_splits(a.m, a.n, a.k, sms);
