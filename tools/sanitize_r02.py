@@ -1,6 +1,6 @@
 """Dev: small launches of every round-2 kernel path for compute-sanitizer (memcheck /
 racecheck / synccheck): batched act quant, exact producers, prefill pair + one-CTA GEMM,
-grouped GEMM, decode kernel (stream-K, cluster, fused XQ)."""
+grouped GEMM, decode kernel (stream-K, ordered stream-K, cluster split-K)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -21,12 +21,15 @@ wq, wsc = fp8q.quantize_weight_blockwise(w)
 for m in (512, 300):  # pair kernel, one-CTA kernel
     a, sa = fp8q.quantize_act_per_token_group(to_dev_bf16(synth.qwen3_activation(m, 1024, 5)))
     fp8q.fp8_block_gemm(a, sa, wq, wsc)
-for m in (1, 5, 8, 40):  # decode: stream-K / cluster, fused XQ at m <= 8
+w2 = to_dev_bf16(synth.qwen3_weight(4096, 1024, 7))
+wq2, ws2 = fp8q.quantize_weight_blockwise(w2)
+w3 = to_dev_bf16(synth.qwen3_weight(128 * 150, 1024, 10))  # 150 tiles: ordered stream-K
+wq3, ws3 = fp8q.quantize_weight_blockwise(w3)
+for m in (1, 5, 8, 40):  # decode: stream-K / cluster split-K / ordered stream-K
     x = to_dev_bf16(synth.qwen3_activation(m, 1024, 6))
     fp8q.fp8_linear_dynamic(x, wq, wsc)
-    w2 = to_dev_bf16(synth.qwen3_weight(4096, 1024, 7))
-    wq2, ws2 = fp8q.quantize_weight_blockwise(w2)
     fp8q.fp8_linear_dynamic(x, wq2, ws2)
+    fp8q.fp8_linear_dynamic(x, wq3, ws3)
 E, n, k = 4, 256, 512
 we = to_dev_bf16(synth.qwen3_weight(E * n, k, 8))
 weq, wes = fp8q.quantize_weight_blockwise(we)
