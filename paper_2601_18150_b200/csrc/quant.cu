@@ -422,27 +422,42 @@ __device__ __forceinline__ void aq_process_item(const AItemRegs& d, uint8_t* __r
 #pragma unroll
         for (int j = 0; j < 4; ++j) ab[j] = max(ab[j], __shfl_xor_sync(0xFFFFFFFFu, ab[j], off));
     }
+    // One vote for the whole item: when every live group of the warp is on the fast path (the
+    // common case) the four groups run as straight-line code, so their table loads, quotients
+    // and stores interleave instead of forming four sequential vote / branch / store sections.
+    bool all_fast = true;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const bool live = chunk * 16u + 4u * j + (lane >> 3) < groups;
+        all_fast = all_fast && (!live || (ab[j] >= kAmaxFastGuardBits && ab[j] < kNonFiniteBits));
+    }
+    float s[4], r[4];
+    uint4 c[4];
+    if (__all_sync(0xFFFFFFFFu, all_fast)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) table_scale_rcp(tabs, ab[j], s[j], r[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = encode16<true>(d.v[j], s[j], r[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool fast = ab[j] >= kAmaxFastGuardBits && ab[j] < kNonFiniteBits;
+            r[j] = 0.0f;
+            if (fast)
+                table_scale_rcp(tabs, ab[j], s[j], r[j]);
+            else
+                s[j] = scale_from_amax_bits(ab[j]);
+            c[j] = fast ? encode16<true>(d.v[j], s[j], r[j]) : encode16<false>(d.v[j], s[j], 0.0f);
+        }
+    }
     uint32_t bad = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const uint32_t g = chunk * 16u + 4u * j + (lane >> 3);
         const bool live = g < groups;
-        const bool fast = ab[j] >= kAmaxFastGuardBits && ab[j] < kNonFiniteBits;
-        float s, r = 0.0f;
-        uint4 c;
-        if (__all_sync(0xFFFFFFFFu, fast || !live)) {  // warp-uniform: the common case
-            table_scale_rcp(tabs, ab[j], s, r);
-            c = encode16<true>(d.v[j], s, r);
-        } else {
-            if (fast)
-                table_scale_rcp(tabs, ab[j], s, r);
-            else
-                s = scale_from_amax_bits(ab[j]);
-            c = fast ? encode16<true>(d.v[j], s, r) : encode16<false>(d.v[j], s, 0.0f);
-        }
-        st_global_f32_if(live && (lane & 7) == 0, srow + static_cast<uint64_t>(g) * ld_s, s);
+        st_global_f32_if(live && (lane & 7) == 0, srow + static_cast<uint64_t>(g) * ld_s, s[j]);
         bad |= (live && ab[j] >= kNonFiniteBits) ? 1u : 0u;
-        st_global_v4_na_if(live, qrow + g * 128 + (lane & 7) * 16, c);
+        st_global_v4_na_if(live, qrow + g * 128 + (lane & 7) * 16, c[j]);
     }
     if (bad && nonfinite_flag != nullptr) *nonfinite_flag = 1;
 }
@@ -479,15 +494,17 @@ __global__ void __launch_bounds__(256, 2) act_per_token_group_wide_kernel(
 
 // ---------------------------------------------------------------------------------------
 // Activations, bulk-staged path (production): one persistent CTA per SM owns an EQUAL
-// contiguous range of items (item = token row x 16 groups = 2048 channels = 4 KB), so no SM
-// finishes a whole item early (the warp-persistent grid above leaves a 1/7 tail at M = 8192,
-// K = 4096).  A producer thread streams the range into a ring of ABQ_STAGES shared-memory stages
-// of ABQ_ITEMS items with cp.async.bulk (one bulk copy per item, completion counted in bytes
-// on the stage's mbarrier): up to ABQ_STAGES x 32 KB of HBM reads in flight per SM, issued by
-// one thread.  Two teams of ABQ_ITEMS consumer warps take alternate stages; each warp encodes
-// one item from shared memory exactly as the wide path does (same registers, same arithmetic)
-// and releases the stage with one arrive.
-constexpr int ABQ_ITEMS = 8;    // items per stage (one per warp of a team)
+// contiguous range of units (unit = 8 token rows x 16 groups = 8 items of 2048 channels = 32 KB),
+// so no SM finishes a whole item early (the warp-persistent grid above leaves a 1/7 tail at
+// M = 8192, K = 4096).  A producer thread streams the range into a ring of ABQ_STAGES shared-
+// memory stages, ONE unit per stage: one 3-D TMA box {128 channels, 16 groups, 8 rows} (rows
+// past m and groups past the row zero-filled, completion counted in bytes on the stage's
+// mbarrier) -- one copy and one barrier arrive per 32 KB, so the single issuing thread is never
+// what paces the stream (with one copy per 4 KB item it was: the consumers waited on the full
+// barriers 40 % of the time at 46 % issue).  Two teams of ABQ_ITEMS consumer warps take
+// alternate stages; warp w encodes row w of the unit from shared memory exactly as the wide
+// path does (same registers, same arithmetic) and releases the stage with one arrive.
+constexpr int ABQ_ITEMS = 8;    // rows per unit = items per stage (one per warp of a team)
 constexpr int ABQ_TEAMS = 2;    // consumer teams (alternate stages)
 constexpr int ABQ_STAGES = 6;   // ring depth: 6 x 32 KB
 constexpr int ABQ_ITEM_BYTES = 4096;
@@ -498,7 +515,15 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
         ::"r"(dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)),
-        "l"(0x12F0000000000000ull)  // L2 evict_first: every byte is read exactly once
+        "l"(kL2EvictFirst)  // every byte is read exactly once
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* smem_dst, const void* desc, uint64_t* bar, int32_t c0,
+                                                 int32_t c1, int32_t c2, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void aq_load_smem(uint32_t base, int64_t groups, int64_t chunk, AItemRegs& d) {
@@ -519,25 +544,26 @@ __device__ __forceinline__ void aq_load_smem(uint32_t base, int64_t groups, int6
     }
 }
 // A batch of activation tensors for one launch of the staged kernel (the four GEMM inputs of a
-// layer in one persistent launch: one pipeline ramp and one tail instead of four).  Items are
-// numbered across the batch (tensor i owns items [item0, item0 + m * chunks)).
+// layer in one persistent launch: one pipeline ramp and one tail instead of four).  Units are
+// numbered across the batch (tensor i owns units [unit0, unit0 + ceil(m / 8) * chunks)), row
+// block major: unit = row block * chunks + chunk.
 struct ATensor {
     const uint16_t* x;
     uint8_t* q;
     float* scales;
     int64_t ld_x, ld_q, ld_s, groups, m;
     int32_t chunks;  // 16-group (4 KB) items per token row
-    int64_t item0;   // first batch-global item of this tensor
+    int64_t unit0;   // first batch-global unit of this tensor
 };
 struct ABatch {
-    CUtensorMap tm[kMaxActBatch];  // kTma: 3-D map {128 channels, groups, m}, box {128, 16, 1}
+    CUtensorMap tm[kMaxActBatch];  // kTma: 3-D map {128 channels, groups, m}, box {128, 16, 8}
     ATensor t[kMaxActBatch];
     int count;
-    int64_t items;
+    int64_t units;
 };
-// kTma: each item is ONE 3-D TMA box (128 BF16 x 16 groups x 1 row of the tensor map
-// {128, groups, m}, groups past the row zero-filled) instead of a cp.async.bulk copy; same
-// shared-memory layout, same consumers.
+// kTma: each unit is ONE 3-D TMA box; !kTma (dev, FP8Q_ACT_LOAD=bulk): one cp.async.bulk copy
+// per live row of the unit.  Same shared-memory layout (row i of the unit at 4 KB * i), same
+// consumers.
 template <bool kTma>
 __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kernel(
     const __grid_constant__ ABatch ab, int32_t* __restrict__ nonfinite_flag) {
@@ -546,19 +572,14 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
     pdl_launch_dependents();
     uint64_t* full = reinterpret_cast<uint64_t*>(abq_smem + size_t(ABQ_STAGES) * ABQ_ITEMS * ABQ_ITEM_BYTES);
     uint64_t* empty = full + ABQ_STAGES;
-    // per item slot: {row, tensor << 16 | chunk}, written by the producer with the copy, so
-    // consumers need no division or tensor search per item
-    __shared__ uint2 meta[ABQ_STAGES * ABQ_ITEMS];
+    // per stage: {first row of the unit, tensor << 16 | chunk}, written by the producer with
+    // the copy, so consumers need no division or tensor search per unit
+    __shared__ uint2 meta[ABQ_STAGES];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // this CTA's equal share of the batch's items
-    const int64_t i0 = ab.items * blockIdx.x / gridDim.x;
-    const int64_t i1 = ab.items * (blockIdx.x + 1) / gridDim.x;
-    const int64_t nstages = (i1 - i0 + ABQ_ITEMS - 1) / ABQ_ITEMS;
-    auto tensor_of = [&](int64_t item) {
-        int i = 0;
-        while (i + 1 < ab.count && item >= ab.t[i + 1].item0) ++i;
-        return i;
-    };
+    // this CTA's equal share of the batch's units
+    const int64_t u0 = ab.units * blockIdx.x / gridDim.x;
+    const int64_t u1 = ab.units * (blockIdx.x + 1) / gridDim.x;
+    const int32_t nstages = static_cast<int32_t>(u1 - u0);
     init_scale_tables(tabs);
     if (threadIdx.x == 0) {
         for (int s = 0; s < ABQ_STAGES; ++s) {
@@ -571,46 +592,45 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
     pdl_wait();  // (no-op unless launched with programmatic stream serialization)
     const uint32_t ring = smem_u32(abq_smem);
     if (warp == ABQ_ITEMS * ABQ_TEAMS) {
-        if (lane == 0 && i1 > i0) {
-            // (tensor, row, chunk) of the current item, advanced incrementally (no 64-bit division
-            // per item)
-            int ti = tensor_of(i0);
-            int64_t row = (i0 - ab.t[ti].item0) / ab.t[ti].chunks;
-            int32_t chunk = static_cast<int32_t>(i0 - ab.t[ti].item0 - row * ab.t[ti].chunks);
-            int64_t left = i1 - i0;
+        if (lane == 0 && nstages > 0) {
+            // (tensor, row block, chunk) of the current unit, advanced incrementally
+            int ti = 0;
+            while (ti + 1 < ab.count && u0 >= ab.t[ti + 1].unit0) ++ti;
+            int32_t chunks = ab.t[ti].chunks;
+            int64_t rows = ab.t[ti].m;
+            int64_t row = ((u0 - ab.t[ti].unit0) / chunks) * ABQ_ITEMS;
+            int32_t chunk = static_cast<int32_t>(u0 - ab.t[ti].unit0 - (row / ABQ_ITEMS) * chunks);
             uint32_t s = 0, ph = 0;
-            while (left > 0) {
+            for (int32_t it = 0; it < nstages; ++it) {
                 mbar_wait(&empty[s], ph ^ 1u);
-                const int cnt = left < ABQ_ITEMS ? static_cast<int>(left) : ABQ_ITEMS;
-                uint32_t bytes = 0;
-                for (int j = 0; j < cnt; ++j) {
+                meta[s] = make_uint2(static_cast<uint32_t>(row),
+                                     (static_cast<uint32_t>(ti) << 16) | static_cast<uint32_t>(chunk));
+                if (kTma) {
+                    // the whole box counts, zero-filled rows / groups included
+                    mbar_arrive_expect_tx(&full[s], ABQ_ITEMS * ABQ_ITEM_BYTES);
+                    tma_load_3d_hint(abq_smem + s * (ABQ_ITEMS * ABQ_ITEM_BYTES), &ab.tm[ti], &full[s], 0, chunk * 16,
+                                     static_cast<int32_t>(row), kL2EvictFirst);
+                } else {
                     const ATensor& t = ab.t[ti];
-                    meta[s * ABQ_ITEMS + j] = make_uint2(static_cast<uint32_t>(row),
-                                                         (static_cast<uint32_t>(ti) << 16) | static_cast<uint32_t>(chunk));
-                    // copies may complete before the expect_tx below: the phase cannot, since
-                    // its one arrival (the expect_tx arrive) is still pending
-                    if (kTma) {
-                        tma_load_3d(abq_smem + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, &ab.tm[ti], &full[s], 0,
-                                    chunk * 16, static_cast<int32_t>(row));
-                        bytes += 4096u;  // the whole box counts, zero-filled groups included
-                    } else {
-                        const uint32_t nb = chunk == t.chunks - 1
-                                                ? static_cast<uint32_t>(t.groups - (t.chunks - 1) * 16) * 256u
-                                                : 4096u;
-                        bulk_g2s(ring + (s * ABQ_ITEMS + j) * ABQ_ITEM_BYTES, t.x + row * t.ld_x + chunk * 2048,
+                    const uint32_t nb = chunk == chunks - 1
+                                            ? static_cast<uint32_t>(t.groups - (chunks - 1) * 16) * 256u
+                                            : 4096u;
+                    const int nr = rows - row < ABQ_ITEMS ? static_cast<int>(rows - row) : ABQ_ITEMS;
+                    mbar_arrive_expect_tx(&full[s], nb * static_cast<uint32_t>(nr));
+                    for (int i = 0; i < nr; ++i)
+                        bulk_g2s(ring + (s * ABQ_ITEMS + i) * ABQ_ITEM_BYTES, t.x + (row + i) * t.ld_x + chunk * 2048,
                                  nb, &full[s]);
-                        bytes += nb;
-                    }
-                    if (++chunk == t.chunks) {
-                        chunk = 0;
-                        if (++row == t.m) {
-                            row = 0;
-                            ++ti;
-                        }
+                }
+                if (++chunk == chunks) {
+                    chunk = 0;
+                    row += ABQ_ITEMS;
+                    if (row >= rows && ti + 1 < ab.count) {
+                        ++ti;
+                        row = 0;
+                        chunks = ab.t[ti].chunks;
+                        rows = ab.t[ti].m;
                     }
                 }
-                mbar_arrive_expect_tx(&full[s], bytes);
-                left -= cnt;
                 if (++s == ABQ_STAGES) {
                     s = 0;
                     ph ^= 1u;
@@ -620,24 +640,29 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
         return;
     }
     const int team = warp / ABQ_ITEMS, w = warp % ABQ_ITEMS;
-    for (int64_t it = team; it < nstages; it += ABQ_TEAMS) {
-        const uint32_t s = static_cast<uint32_t>(it % ABQ_STAGES);
-        mbar_wait(&full[s], static_cast<uint32_t>((it / ABQ_STAGES) & 1));
-        const int64_t item = i0 + it * ABQ_ITEMS + w;
-        if (item < i1) {
-            const uint2 md = meta[s * ABQ_ITEMS + w];
-            const ATensor& t = ab.t[md.y >> 16];
+    uint32_t s = static_cast<uint32_t>(team), ph = 0;
+    for (int32_t it = team; it < nstages; it += ABQ_TEAMS) {
+        mbar_wait(&full[s], ph);
+        const uint2 md = meta[s];
+        const ATensor& t = ab.t[md.y >> 16];
+        const uint32_t row = md.x + static_cast<uint32_t>(w);
+        if (row < static_cast<uint64_t>(t.m)) {
             const uint32_t chunk = md.y & 0xFFFFu;
             const uint32_t groups = static_cast<uint32_t>(t.groups);
             AItemRegs d;
             aq_load_smem(ring + (s * ABQ_ITEMS + w) * ABQ_ITEM_BYTES, groups, chunk, d);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);  // the item is in registers: free the slot
-            aq_process_item(d, t.q + int64_t(md.x) * t.ld_q, t.scales + md.x, static_cast<uint32_t>(t.ld_s), groups,
+            if (lane == 0) mbar_arrive(&empty[s]);  // the row is in registers: free the slot
+            aq_process_item(d, t.q + int64_t(row) * t.ld_q, t.scales + row, static_cast<uint32_t>(t.ld_s), groups,
                             chunk, nonfinite_flag, tabs);
         } else {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        s += ABQ_TEAMS;
+        if (s >= ABQ_STAGES) {
+            s -= ABQ_STAGES;
+            ph ^= 1u;
         }
     }
 }
@@ -735,7 +760,7 @@ __global__ void __launch_bounds__(WBQ_THREADS, 1) weight_blockwise_bulk_kernel(c
             mbar_arrive_expect_tx(&full[s], WBQ_BLOCK_BYTES);
             tma_load_2d_hint(wbq_smem + size_t(s) * WBQ_BLOCK_BYTES, &bt.tm[ti], &full[s],
                              static_cast<int32_t>(bj * 128), static_cast<int32_t>(bi * 128),
-                             0x12F0000000000000ull);  // L2 evict_first: every byte is read once
+                             kL2EvictFirst);  // every byte is read once
             if (++bj == t.nbk) {
                 bj = 0;
                 if (++bi * 128 >= t.n) {
@@ -1002,15 +1027,15 @@ cudaError_t launch_act_batch(const ActDesc* descs, int count, int32_t* flag, cud
     const bool use_tma = act_tma_env && encode != nullptr;
     ABatch ab{};
     ab.count = 0;
-    ab.items = 0;
+    ab.units = 0;
     auto flush = [&]() -> cudaError_t {
-        if (ab.count == 0 || ab.items == 0) {
+        if (ab.count == 0 || ab.units == 0) {
             ab.count = 0;
-            ab.items = 0;
+            ab.units = 0;
             return cudaSuccess;
         }
-        const int64_t per_cta_min = 2 * ABQ_ITEMS;  // small inputs: fewer CTAs, each a few stages
-        int64_t grid = (ab.items + per_cta_min - 1) / per_cta_min;
+        const int64_t per_cta_min = 2;  // small inputs: fewer CTAs, each a few stages
+        int64_t grid = (ab.units + per_cta_min - 1) / per_cta_min;
         grid = grid < sm_count() ? grid : sm_count();
         const cudaError_t e =
             use_tma ? launch_pdl(act_per_token_group_bulk_kernel<true>, static_cast<unsigned>(grid), ABQ_THREADS,
@@ -1019,7 +1044,7 @@ cudaError_t launch_act_batch(const ActDesc* descs, int count, int32_t* flag, cud
                                  ABQ_SMEM, stream, ab, flag);
         if (e != cudaSuccess) return e;
         ab.count = 0;
-        ab.items = 0;
+        ab.units = 0;
         return cudaGetLastError();
     };
     for (int i = 0; i < count; ++i) {
@@ -1044,18 +1069,18 @@ cudaError_t launch_act_batch(const ActDesc* descs, int count, int32_t* flag, cud
         t.groups = groups;
         t.m = d.m;
         t.chunks = static_cast<int32_t>((groups + 15) / 16);
-        t.item0 = ab.items;
+        t.unit0 = ab.units;
         if (use_tma) {
             cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(groups), static_cast<cuuint64_t>(d.m)};
             cuuint64_t strides[2] = {256, static_cast<cuuint64_t>(d.ld_x) * 2};
-            cuuint32_t box[3] = {128, 16, 1};
+            cuuint32_t box[3] = {128, 16, static_cast<cuuint32_t>(ABQ_ITEMS)};
             cuuint32_t estr[3] = {1, 1, 1};
             if (encode(&ab.tm[ab.count], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(d.x), dims,
                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
                 return cudaErrorInvalidValue;
         }
-        ab.items += d.m * t.chunks;
+        ab.units += ((d.m + ABQ_ITEMS - 1) / ABQ_ITEMS) * t.chunks;
         if (++ab.count == kMaxActBatch) {
             cudaError_t e = flush();
             if (e != cudaSuccess) return e;
