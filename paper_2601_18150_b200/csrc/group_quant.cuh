@@ -45,14 +45,13 @@ __device__ __forceinline__ uint32_t abs_max_bits16(const uint32_t (&w)[8]) {
                        0x7FFF7FFFu;
     return max(a & 0xFFFFu, a >> 16);
 }
-// 16 BF16 (8 words) -> 16 E4M3 codes (4 words).
-template <bool kFast>
-__device__ __forceinline__ uint4 encode16(const uint32_t (&w)[8], float s, float r) {
+// 2 NW BF16 (NW words) -> 2 NW E4M3 codes (NW / 2 words).
+template <bool kFast, int NW>
+__device__ __forceinline__ void encode_words(const uint32_t* w, float s, float r, uint32_t* c) {
     const uint64_t rr = pack2(r, r);
     const uint64_t nss = pack2(-s, -s);
-    uint32_t c[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NW / 2; ++i) {
         const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
         float q0, q1, q2, q3;
         if (kFast) {
@@ -71,7 +70,20 @@ __device__ __forceinline__ uint4 encode16(const uint32_t (&w)[8], float s, float
         const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;  // input sign bits
         c[i] = (cvt_e4m3x2(q0, q1) | (cvt_e4m3x2(q2, q3) << 16)) | sign;
     }
+}
+// 16 BF16 (8 words) -> 16 E4M3 codes (4 words).
+template <bool kFast>
+__device__ __forceinline__ uint4 encode16(const uint32_t (&w)[8], float s, float r) {
+    uint32_t c[4];
+    encode_words<kFast, 8>(w, s, r, c);
     return make_uint4(c[0], c[1], c[2], c[3]);
+}
+// 8 BF16 (4 words) -> 8 E4M3 codes (2 words), the same operations per element.
+template <bool kFast>
+__device__ __forceinline__ uint2 encode8w(const uint32_t (&w)[4], float s, float r) {
+    uint32_t c[2];
+    encode_words<kFast, 4>(w, s, r, c);
+    return make_uint2(c[0], c[1]);
 }
 
 }  // namespace fp8q

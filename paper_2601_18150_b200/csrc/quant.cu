@@ -685,50 +685,27 @@ constexpr int WBQ_BLOCK_BYTES = 128 * 256;
 constexpr int WBQ_THREADS = (8 * WBQ_TEAMS + 1) * 32;
 constexpr size_t WBQ_SMEM = size_t(WBQ_STAGES) * WBQ_BLOCK_BYTES + 2 * WBQ_STAGES * 8 + 128;
 
-// Thread (warp w of its team, lane l) takes rows 16w + 4i + (l >> 3), columns 16 (l & 7) .. +15
-// of the staged block (row r at byte 256 r): the 16-byte chunks 2j and 2j+1 (j = l & 7).  The
-// two loads visit them in the order (2j + h, 2j + 1 - h), h = j >> 2, so each 8-lane phase
-// touches 8 distinct bank quads (chunk mod 8 all different): conflict-free.
-__device__ __forceinline__ void wq_load_smem(uint32_t base, int64_t rows_in, int64_t cols_in, int warp,
-                                             WBlockRegs& d) {
-    const int lane = threadIdx.x & 31, j = lane & 7, h = j >> 2;
-    const bool col_ok = 16 * j < cols_in;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int r = warp * 16 + 4 * i + (lane >> 3);
-        if (col_ok && r < rows_in) {
-            const uint32_t a = base + static_cast<uint32_t>(r * 256);
-            uint32_t p0, p1, p2, p3, q0, q1, q2, q3;
-            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(p0), "=r"(p1), "=r"(p2), "=r"(p3) : "r"(a + (2 * j + h) * 16));
-            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(q0), "=r"(q1), "=r"(q2), "=r"(q3) : "r"(a + (2 * j + 1 - h) * 16));
-            d.v[i][0] = h ? q0 : p0;
-            d.v[i][1] = h ? q1 : p1;
-            d.v[i][2] = h ? q2 : p2;
-            d.v[i][3] = h ? q3 : p3;
-            d.v[i][4] = h ? p0 : q0;
-            d.v[i][5] = h ? p1 : q1;
-            d.v[i][6] = h ? p2 : q2;
-            d.v[i][7] = h ? p3 : q3;
-        } else {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) d.v[i][t] = 0u;
-        }
-    }
-}
-
+// Consumer side of the staged weight kernel.  Thread (warp w of its team, lane l) takes the
+// 8-element segment l & 15 (16 B at byte 16 (l & 15)) of rows 16 w + 2 i + (l >> 4), i = 0..7:
+// each LDS.128 of a warp reads two full 256-byte rows (every 8-lane phase 128 contiguous bytes:
+// conflict-free, no lane permutation), and each 8-byte code store of a warp writes two full
+// 128-byte code rows.  The tensor map zero-fills rows past n and columns past k, so the loads
+// need no masks (zeros never raise the amax); the producer hands over (block row, block
+// column, tensor) with the stage, so the consumers do no 64-bit division or tensor search.
 template <bool kFanout>
 __global__ void __launch_bounds__(WBQ_THREADS, 1) weight_blockwise_bulk_kernel(const __grid_constant__ WBatch bt,
                                                                                int32_t* __restrict__ nonfinite_flag) {
     extern __shared__ __align__(128) uint8_t wbq_smem[];
     __shared__ uint32_t red[WBQ_TEAMS][2][8];
+    __shared__ uint2 wmeta[WBQ_STAGES];  // {block row, tensor << 24 | block column}
+    __shared__ ScaleTables tabs;
     uint64_t* full = reinterpret_cast<uint64_t*>(wbq_smem + size_t(WBQ_STAGES) * WBQ_BLOCK_BYTES);
     uint64_t* empty = full + WBQ_STAGES;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b0 = bt.nblocks * blockIdx.x / gridDim.x;
     const int64_t b1 = bt.nblocks * (blockIdx.x + 1) / gridDim.x;
-    const int64_t nb = b1 - b0;
+    const int32_t nb = static_cast<int32_t>(b1 - b0);
+    init_scale_tables(tabs);
     if (threadIdx.x == 0) {
         for (int s = 0; s < WBQ_STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -738,34 +715,31 @@ __global__ void __launch_bounds__(WBQ_THREADS, 1) weight_blockwise_bulk_kernel(c
     }
     __syncthreads();
     const uint32_t ring = smem_u32(wbq_smem);
-    auto tensor_of = [&](int64_t blk) {
-        int i = 0;
-        while (i + 1 < bt.count && blk >= bt.t[i + 1].blk0) ++i;
-        return i;
-    };
     if (warp == 8 * WBQ_TEAMS) {  // producer warp (one elected lane)
-        if (lane != 0) return;
-        int ti = nb > 0 ? tensor_of(b0) : 0;
-        int64_t bi = 0, bj = 0;
-        if (nb > 0) {
-            const int64_t local = b0 - bt.t[ti].blk0;
-            bi = local / bt.t[ti].nbk;
-            bj = local - bi * bt.t[ti].nbk;
-        }
+        if (lane != 0 || nb <= 0) return;
+        int ti = 0;
+        while (ti + 1 < bt.count && b0 >= bt.t[ti + 1].blk0) ++ti;
+        const int64_t local = b0 - bt.t[ti].blk0;
+        uint32_t bi = static_cast<uint32_t>(local / bt.t[ti].nbk);
+        uint32_t bj = static_cast<uint32_t>(local - int64_t(bi) * bt.t[ti].nbk);
+        uint32_t nbk = static_cast<uint32_t>(bt.t[ti].nbk);
+        int64_t n = bt.t[ti].n;
         uint32_t s = 0, ph = 0;
-        for (int64_t it = 0; it < nb; ++it) {
-            const WTensor& t = bt.t[ti];
+        for (int32_t it = 0; it < nb; ++it) {
             mbar_wait(&empty[s], ph ^ 1u);
+            wmeta[s] = make_uint2(bi, (static_cast<uint32_t>(ti) << 24) | bj);
             // the full box is counted even where it is zero-filled out of bounds
             mbar_arrive_expect_tx(&full[s], WBQ_BLOCK_BYTES);
             tma_load_2d_hint(wbq_smem + size_t(s) * WBQ_BLOCK_BYTES, &bt.tm[ti], &full[s],
                              static_cast<int32_t>(bj * 128), static_cast<int32_t>(bi * 128),
                              kL2EvictFirst);  // every byte is read once
-            if (++bj == t.nbk) {
+            if (++bj == nbk) {
                 bj = 0;
-                if (++bi * 128 >= t.n) {
+                if (int64_t(++bi) * 128 >= n && ti + 1 < bt.count) {
                     bi = 0;
                     ++ti;
+                    nbk = static_cast<uint32_t>(bt.t[ti].nbk);
+                    n = bt.t[ti].n;
                 }
             }
             if (++s == WBQ_STAGES) {
@@ -776,21 +750,73 @@ __global__ void __launch_bounds__(WBQ_THREADS, 1) weight_blockwise_bulk_kernel(c
         return;
     }
     const int team = warp >> 3, w = warp & 7;
+    const uint32_t seg = static_cast<uint32_t>(lane & 15);
+    const uint32_t r0 = static_cast<uint32_t>(w * 16 + (lane >> 4));  // first of this thread's rows
     int par = 0;
-    for (int64_t it = team; it < nb; it += WBQ_TEAMS) {
-        const uint32_t s = static_cast<uint32_t>(it % WBQ_STAGES);
-        const int64_t blk = b0 + it;
-        const WTensor& t = bt.t[tensor_of(blk)];
-        const int64_t local = blk - t.blk0;
-        const int64_t bi = local / t.nbk, bj = local - (local / t.nbk) * t.nbk;
-        mbar_wait(&full[s], static_cast<uint32_t>((it / WBQ_STAGES) & 1));
-        WBlockRegs d;
-        wq_load_smem(ring + s * WBQ_BLOCK_BYTES, t.n - bi * 128, t.k - bj * 128, w, d);
+    uint32_t s = static_cast<uint32_t>(team), ph = 0;
+    for (int32_t it = team; it < nb; it += WBQ_TEAMS) {
+        mbar_wait(&full[s], ph);
+        const uint2 md = wmeta[s];
+        uint32_t v[8][4];
+        const uint32_t src = ring + s * WBQ_BLOCK_BYTES + r0 * 256u + seg * 16u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v[i][0]), "=r"(v[i][1]), "=r"(v[i][2]), "=r"(v[i][3]) : "r"(src + i * 512u));
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // the block is in registers: free the stage
-        wq_process<kFanout>(d, t.n, t.k, t.q, t.ld_q, t.scales, t.ld_s, t.nbk, local, red[team][par],
-                            nonfinite_flag, bt, w, 1 + team);
+        // block amax: max over sign-cleared BF16 bits (reading Q2), lanes, then the team's 8 warps
+        uint32_t m2[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m2[i] = bmax_abs2(bmax_abs2(v[i][0], v[i][1]), bmax_abs2(v[i][2], v[i][3]));
+        uint32_t a2 = bmax_abs2(bmax_abs2(bmax_abs2(m2[0], m2[1]), bmax_abs2(m2[2], m2[3])),
+                                bmax_abs2(bmax_abs2(m2[4], m2[5]), bmax_abs2(m2[6], m2[7]))) &
+                      0x7FFF7FFFu;
+        uint32_t ab = __reduce_max_sync(0xFFFFFFFFu, max(a2 & 0xFFFFu, a2 >> 16));
+        if (lane == 0) red[team][par][w] = ab;
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + team) : "memory");
+        ab = red[team][par][0];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) ab = max(ab, red[team][par][i]);
+        const WTensor& t = bt.t[md.y >> 24];
+        const uint32_t bi = md.x, bj = md.y & 0xFFFFFFu;
+        const bool fast = ab >= kAmaxFastGuardBits && ab < kNonFiniteBits;  // block-uniform
+        float sc, rc = 0.0f;
+        if (fast)
+            table_scale_rcp(tabs, ab, sc, rc);
+        else
+            sc = scale_from_amax_bits(ab);
+        if (w == 0 && lane == 0) {
+            float* sp = t.scales + int64_t(bi) * t.ld_s + bj;
+            if (kFanout) {
+                for (int dd = 0; dd < bt.ndest; ++dd)
+                    *reinterpret_cast<float*>(reinterpret_cast<char*>(sp) + bt.ds[dd]) = sc;
+            } else {
+                *sp = sc;
+            }
+            if (ab >= kNonFiniteBits && nonfinite_flag != nullptr) *nonfinite_flag = 1;
+        }
+        const int64_t rows_left = t.n - int64_t(bi) * 128;
+        const bool col_ok = int64_t(bj) * 128 + seg * 8 < t.k;
+        uint8_t* qb = t.q + (int64_t(bi) * 128 + r0) * t.ld_q + int64_t(bj) * 128 + seg * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint2 c = fast ? encode8w<true>(v[i], sc, rc) : encode8w<false>(v[i], sc, 0.0f);
+            if (col_ok && int64_t(r0) + 2 * i < rows_left) {
+                uint8_t* dst = qb + int64_t(2 * i) * t.ld_q;
+                if (kFanout) {
+                    for (int dd = 0; dd < bt.ndest; ++dd) st_stream_v2(dst + bt.dq[dd], c.x, c.y);
+                } else {
+                    st_stream_v2(dst, c.x, c.y);
+                }
+            }
+        }
         par ^= 1;
+        s += WBQ_TEAMS;
+        if (s >= WBQ_STAGES) {
+            s -= WBQ_STAGES;
+            ph ^= 1u;
+        }
     }
 }
 
