@@ -20,9 +20,15 @@ def main(path, regex, skip=0):
     i_src, i_ex, i_s = h.index("Source"), h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
     ops, samp, tot, stot = collections.Counter(), collections.Counter(), 0, 0
     lines = []
+    i_addr = h.index("Address") if "Address" in h else None
+    seen = set()
     for x in body:
         if len(x) <= i_ex or not x[i_ex].isdigit():
             continue
+        if i_addr is not None:  # the source page can list a SASS line more than once
+            if x[i_addr] in seen:
+                continue
+            seen.add(x[i_addr])
         e, sm, src = int(x[i_ex]), int(x[i_s]) if x[i_s].isdigit() else 0, x[i_src].strip()
         op = re.sub(r"^@!?U?P\w+\s+", "", src).split()[0].split(".")[0] if src else "?"
         ops[op] += e
