@@ -163,6 +163,24 @@ def test_act_prefill_full_size():
     _assert_act_exact(synth.qwen3_activation(8192, 4096, 0))
 
 
+@pytest.mark.parametrize("m,k,kind", [(257, 2176, "uniform"), (300, 384, "zeros"), (1000, 128, "qwen"),
+                                      (513, 12288, "qwen"), (263, 1024, "uniform")])
+def test_act_staged_ragged_rows_and_groups(m, k, kind):
+    # > 256 tokens: the TMA-staged kernel (one 3-D box of 8 token rows x 16 groups per ring stage);
+    # token counts that are not a multiple of 8 (the last unit's rows past m are zero-filled and
+    # skipped) and group counts that are not a multiple of 16 (zero-filled groups), with full-range
+    # bit patterns and zero / negative-zero rows
+    if kind == "uniform":
+        bits = synth.uniform_bits((m, k), 31 + m)
+    else:
+        bits = synth.qwen3_activation(m, k, 41 + m)
+    if kind == "zeros":
+        bits[::7, :] = 0
+        bits[3::7, :] = 0x8000
+        bits[5, 5] = 0x0001
+    _assert_act_exact(bits, ld_pad=4)
+
+
 def test_act_zero_and_signed_zero_rows():
     bits = np.zeros((4, 256), np.uint16)
     bits[1, :] = 0x8000
