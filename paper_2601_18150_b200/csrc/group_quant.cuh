@@ -46,29 +46,33 @@ __device__ __forceinline__ uint32_t abs_max_bits16(const uint32_t (&w)[8]) {
     return max(a & 0xFFFFu, a >> 16);
 }
 // 2 NW BF16 (NW words) -> 2 NW E4M3 codes (NW / 2 words).
+// Fast path: the guarded Markstein quotient evaluated NEGATED, -q1 = fma(e, -r, -q0) with
+// -q0 = x (-r) and e = fma(-q0, s, x) (the same e as fma(q0, -s, x); every step is the exact
+// negation of the unnegated one, RN being sign-symmetric), then code(q1) = code(-q1) ^ 0x80.
+// The negated form gets the sign of a zero quotient right by itself (x = -0: -q0 = +0, e = +0,
+// -q1 = +0 -> 0x80; x = +0: -q1 = -0 -> 0x00), so the input sign bits need not be gathered.
 template <bool kFast, int NW>
 __device__ __forceinline__ void encode_words(const uint32_t* w, float s, float r, uint32_t* c) {
-    const uint64_t rr = pack2(r, r);
-    const uint64_t nss = pack2(-s, -s);
+    const uint64_t nrr = pack2(-r, -r);
+    const uint64_t ss = pack2(s, s);
 #pragma unroll
     for (int i = 0; i < NW / 2; ++i) {
         const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
-        float q0, q1, q2, q3;
         if (kFast) {
-            const uint64_t qa = quot2_fast(pack2(__uint_as_float(wa << 16), __uint_as_float(wa & 0xFFFF0000u)), rr, nss);
-            const uint64_t qb = quot2_fast(pack2(__uint_as_float(wb << 16), __uint_as_float(wb & 0xFFFF0000u)), rr, nss);
-            q0 = lo_of(qa);
-            q1 = hi_of(qa);
-            q2 = lo_of(qb);
-            q3 = hi_of(qb);
+            const uint64_t xa = pack2(__uint_as_float(wa << 16), __uint_as_float(wa & 0xFFFF0000u));
+            const uint64_t xb = pack2(__uint_as_float(wb << 16), __uint_as_float(wb & 0xFFFF0000u));
+            const uint64_t na = mul2(xa, nrr), nb = mul2(xb, nrr);  // -q0
+            const uint64_t ea = fma2(na, ss, xa), eb = fma2(nb, ss, xb);  // e = x - q0 s
+            const uint64_t qa = fma2(ea, nrr, na), qb = fma2(eb, nrr, nb);  // -q1 = -(q0 + e r)
+            c[i] = (cvt_e4m3x2(lo_of(qa), hi_of(qa)) | (cvt_e4m3x2(lo_of(qb), hi_of(qb)) << 16)) ^ 0x80808080u;
         } else {
-            q0 = __fdiv_rn(__uint_as_float(wa << 16), s);
-            q1 = __fdiv_rn(__uint_as_float(wa & 0xFFFF0000u), s);
-            q2 = __fdiv_rn(__uint_as_float(wb << 16), s);
-            q3 = __fdiv_rn(__uint_as_float(wb & 0xFFFF0000u), s);
+            const float q0 = __fdiv_rn(__uint_as_float(wa << 16), s);
+            const float q1 = __fdiv_rn(__uint_as_float(wa & 0xFFFF0000u), s);
+            const float q2 = __fdiv_rn(__uint_as_float(wb << 16), s);
+            const float q3 = __fdiv_rn(__uint_as_float(wb & 0xFFFF0000u), s);
+            const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;  // input sign bits
+            c[i] = (cvt_e4m3x2(q0, q1) | (cvt_e4m3x2(q2, q3) << 16)) | sign;
         }
-        const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;  // input sign bits
-        c[i] = (cvt_e4m3x2(q0, q1) | (cvt_e4m3x2(q2, q3) << 16)) | sign;
     }
 }
 // 16 BF16 (8 words) -> 16 E4M3 codes (4 words).
