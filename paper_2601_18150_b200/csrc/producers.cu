@@ -26,6 +26,7 @@
 #include <cstdint>
 #include <mutex>
 
+#include "group_quant.cuh"
 #include "packed.cuh"
 #include "pdl.cuh"
 #include "ptx.cuh"
@@ -46,37 +47,8 @@ __device__ __forceinline__ uint32_t absmax_bits8(const uint4& v) {
 __device__ __forceinline__ float scale_of(uint32_t ab) {
     return ab == 0u ? 1.0f : __fdiv_rn(__uint_as_float(ab << 16), 448.0f);
 }
-// 8 BF16 (4 words) -> 8 codes (2 words); sign bits OR-ed in (restores -0, no-op otherwise).
-// Fast path: the pair Markstein quotient; slow path (amax < 2^-104 or non-finite): div.rn.
-__device__ __forceinline__ uint2 encode8_fast(const uint4& v, float s, float r) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    const uint64_t rr = pack2(r, r), nss = pack2(-s, -s);
-    uint32_t c[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
-        const uint64_t qa = quot2_fast(bf16x2_to_f32x2(wa), rr, nss);
-        const uint64_t qb = quot2_fast(bf16x2_to_f32x2(wb), rr, nss);
-        const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;
-        c[i] = (cvt_e4m3x2(lo_of(qa), hi_of(qa)) | (cvt_e4m3x2(lo_of(qb), hi_of(qb)) << 16)) | sign;
-    }
-    return make_uint2(c[0], c[1]);
-}
-__device__ __noinline__ uint2 encode8_slow(const uint4& v, float s) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    uint32_t c[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
-        const float q0 = __fdiv_rn(__uint_as_float(wa << 16), s);
-        const float q1 = __fdiv_rn(__uint_as_float(wa & 0xFFFF0000u), s);
-        const float q2 = __fdiv_rn(__uint_as_float(wb << 16), s);
-        const float q3 = __fdiv_rn(__uint_as_float(wb & 0xFFFF0000u), s);
-        const uint32_t sign = __byte_perm(wa, wb, 0x7531) & 0x80808080u;
-        c[i] = (cvt_e4m3x2(q0, q1) | (cvt_e4m3x2(q2, q3) << 16)) | sign;
-    }
-    return make_uint2(c[0], c[1]);
-}
+// 8 BF16 (4 words) -> 8 codes (2 words): the quantizers' element map (group_quant.cuh) --
+// fast path the negated pair Markstein quotient, slow path (amax < 2^-104 or non-finite) div.rn.
 // The amax of this lane's half-warp group (lanes 0-15 / 16-31 hold one 128-channel group each).
 __device__ __forceinline__ uint32_t group_amax(uint32_t ab) {
 #pragma unroll
@@ -97,7 +69,8 @@ __device__ __forceinline__ uint2 quantize8(const uint4& y, uint32_t ab, int lane
         *scale_dst = s;
         if (ab >= kNonFinite && flag != nullptr) *flag = 1;
     }
-    return fast ? encode8_fast(y, s, r) : encode8_slow(y, s);
+    const uint32_t w[4] = {y.x, y.y, y.z, y.w};
+    return fast ? encode8w<true>(w, s, r) : encode8w<false>(w, s, 0.0f);
 }
 __device__ __forceinline__ uint4 ld_nc(const void* p) {
     uint4 r;
