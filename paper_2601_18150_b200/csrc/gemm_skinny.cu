@@ -119,6 +119,7 @@ struct SkParams {
     int64_t total;      // T = tiles * num_kb
     float* ws;          // stream-K partials: two [MT][128] fp32 slots per CTA
     int32_t* counters;  // [tiles], left zeroed
+    int prefetch;       // weight stages issued before griddepcontrol.wait (dev A/B: FP8Q_SKINNY_PREFETCH)
 };
 __device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -300,15 +301,18 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             SegIter seg;
             seg.init(p);
             int tile, kb0, kb1;
+            uint32_t npf = 0;  // weight stages already in flight
             {
                 SegIter pre = seg;
                 int pt, pk0, pk1;
                 uint32_t n = 0;
-                while (n < STAGES && pre.next(p, pt, pk0, pk1))
-                    for (int kb = pk0; kb < pk1 && n < STAGES; ++kb, ++n) {
+                const uint32_t cap = min(static_cast<uint32_t>(STAGES), static_cast<uint32_t>(p.prefetch));
+                while (n < cap && pre.next(p, pt, pk0, pk1))
+                    for (int kb = pk0; kb < pk1 && n < cap; ++kb, ++n) {
                         mbar_arrive_expect_tx(&full[n], C::TX_BYTES);
                         tma_load_2d(smW + n * C::W_TILE, &tmW, &full[n], kb * SK_BK, pt * SK_BN);
                     }
+                npf = n;
             }
             grid_dependency_wait();
             FP8Q_TREC(trace_tag, 1);
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
-                    const bool prefetched = it < STAGES;  // W already in flight, expect_tx armed
+                    const bool prefetched = it < npf;  // W already in flight, expect_tx armed
                     if (!prefetched) {
                         mbar_wait(&empty[stage], ph ^ 1u);
                         mbar_wait(&sempty[stage], ph ^ 1u);
@@ -761,6 +765,17 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     p.total = int64_t(p.tiles) * p.num_kb;
     p.streamk = 0;
     p.cs = 1;
+    // Weight stages issued before griddepcontrol.wait.  Measured (decode layer, A/B x2, session 3):
+    // the whole ring (11 stages at M = 1, 19 MB over 96 SMs for qkv) saturates HBM while the
+    // preceding activation quantizer waits for its own (tiny) input behind it, so that
+    // quantizer's load latency grew to ~3 us; 4 stages: M = 1 layer 66.5 -> 64.8 us, M = 64
+    // 79.6 -> 78.5, M >= 128 unchanged (0 / 2 / 6 stages: 68.8 / 66.6 / 64.5 at M = 1).
+    // Dev A/B: FP8Q_SKINNY_PREFETCH=n.
+    static const int prefetch = [] {
+        const char* e = std::getenv("FP8Q_SKINNY_PREFETCH");
+        return e ? std::atoi(e) : 4;
+    }();
+    p.prefetch = prefetch;
     p.ws = nullptr;
     p.counters = nullptr;
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, sms));  // whole tiles
