@@ -240,10 +240,14 @@ fp8q_status fp8_block_gemm(const uint8_t* a, int64_t ld_a, const float* a_scales
  *   workspace / workspace_bytes: at least fp8_linear_dynamic_workspace_size(m, n, k) bytes,
  *     256-byte aligned, ZERO-FILLED before first use (the GEMM's split-K counters; every launch
  *     leaves them zeroed), holding the activation codes and scales between the two kernels
- *     (FP8Q_EWORKSPACE if missing or too small).  The quantizer is launched with programmatic
+ *     (FP8Q_EWORKSPACE if missing or too small).  At m <= 16 where the decode kernel applies
+ *     (and its CTAs' activation k-blocks fit 32 shared-memory slots: every Qwen3-8B linear), ONE
+ *     launch: the decode GEMM's promotion warps quantize the BF16 rows of the CTA's k-blocks into
+ *     shared memory after griddepcontrol.wait, with the quantizers' element map (the codes and
+ *     scales never reach the workspace).  Otherwise the quantizer is launched with programmatic
  *     dependent launch and, for <= 256 tokens, as a shared-memory-free kernel, so the decode
- *     GEMM's weight prefetch overlaps it.  (Round 2 also built a single-kernel form -- the decode
- *     GEMM quantizing its activations itself: slower than this pair, removed.)
+ *     GEMM's weight prefetch overlaps it.  (round 2's single-kernel form, which
+ *     quantized per k-block through the ring, was slower than the pair and removed.)
  *   Requirements as fp8_block_gemm (k % 128, n % 8, alignments).
  */
 size_t fp8_linear_dynamic_workspace_size(int64_t m, int64_t n, int64_t k);

@@ -471,6 +471,36 @@ fp8q_status fp8_linear_dynamic(const void* x_bf16, int64_t ld_x, const uint8_t* 
     if (workspace == nullptr || workspace_bytes < fp8_linear_dynamic_workspace_size(m, n, k)) return FP8Q_EWORKSPACE;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t gws = fp8q::gemm_workspace_bytes(m, n, k, false);
+    {
+        // decode sizes: the GEMM kernel quantizes the activations itself (one launch)
+        fp8q::GemmArgs f{};
+        f.a = nullptr;
+        f.ld_a = k;
+        f.sa = nullptr;
+        f.ld_sa = act_ld_s(m);
+        f.b = b;
+        f.ld_b = ld_b;
+        f.sb = b_scales;
+        f.ld_sb = ld_sb;
+        f.d = d;
+        f.ld_d = ld_d;
+        f.out_f32 = d_dtype == FP8Q_OUT_F32;
+        f.m = m;
+        f.n = n;
+        f.k = k;
+        f.groups = 1;
+        f.workspace = gws > 0 ? workspace : nullptr;
+        f.workspace_bytes = gws;
+        f.x_bf16 = static_cast<const uint16_t*>(x_bf16);
+        f.ld_x = ld_x;
+        f.nonfinite_flag = nonfinite_flag;
+        if (fp8q::skinny_fused_act_applies(f)) {
+            int launched = 0;
+            const cudaError_t ef = fp8q::launch_fp8_block_gemm(f, s, &launched);
+            g_launches.fetch_add(launched);
+            return from_cuda(ef);
+        }
+    }
     char* base = static_cast<char*>(workspace);
     const size_t off = act_codes_offset(m, n, k);
     uint8_t* codes = reinterpret_cast<uint8_t*>(base + off);

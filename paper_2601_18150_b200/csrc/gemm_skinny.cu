@@ -54,8 +54,10 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "group_quant.cuh"
 #include "ptx.cuh"
 #include "quant_kernels.h"
+#include "scale_tables.cuh"
 #include "trace.cuh"
 
 namespace fp8q {
@@ -102,6 +104,21 @@ struct SkCfg {
     static_assert(STAGES * (W_TILE + X_TILE) >= MT * SK_BN * 4, "no room for the cluster split-K partial");
 };
 
+// Fused activation quantization (fp8_linear_dynamic at m <= 16, MT = 16): the ring carries only
+// weight tiles; the CTA's activation codes live in a persistent region of up to kFxSlots
+// k-blocks (16 rows x 128 B each, SW128 layout) with their scales, written once by the
+// promotion warps after griddepcontrol.wait (no separate quantizer launch, no global round trip).
+constexpr int kFxSlots = 32;
+struct SkFxCfg {
+    static constexpr int MT = 16;
+    static constexpr int W_TILE = SK_BN * SK_BK;
+    static constexpr int X_SLOT = MT * SK_BK;  // 2 KB
+    static constexpr int STAGES = 8;
+    static constexpr size_t SMEM_BYTES =
+        1024 + size_t(STAGES) * W_TILE + size_t(kFxSlots) * X_SLOT + kFxSlots * MT * 4 + 512;
+    static_assert(STAGES * W_TILE >= MT * SK_BN * 4, "no room for the cluster split-K partial");
+};
+
 struct SkParams {
     const float* sb;
     int64_t ld_sb;
@@ -120,6 +137,9 @@ struct SkParams {
     float* ws;          // stream-K partials: two [MT][128] fp32 slots per CTA
     int32_t* counters;  // [tiles], left zeroed
     int prefetch;       // weight stages issued before griddepcontrol.wait (dev A/B: FP8Q_SKINNY_PREFETCH)
+    const uint16_t* x;  // fused activation quantization: BF16 activations [m][ld_x] (else null)
+    int64_t ld_x;
+    int32_t* flag;      // non-finite flag of the fused quantization (nullable)
 };
 __device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -241,28 +261,61 @@ __device__ __forceinline__ void sk_store(const SkParams& p, int64_t n_row, int j
     }
 }
 
-template <int MT>
+// The CTA's activation k-blocks in the fused mode: [kx0, kx0 + nkx) (the host guarantees
+// nkx <= kFxSlots); a range that crosses a tile boundary takes all k-blocks.
+__device__ __forceinline__ void sk_fx_range(const SkParams& p, int& kx0, int& nkx) {
+    if (p.streamk == 2) {
+        const int r = static_cast<int>(cluster_ctarank());
+        kx0 = r * p.num_kb / p.cs;
+        nkx = (r + 1) * p.num_kb / p.cs - kx0;
+    } else if (p.streamk == 1 || p.streamk == 3) {
+        const int64_t x = static_cast<int64_t>(blockIdx.x) * p.total / gridDim.x;
+        const int64_t e = static_cast<int64_t>(blockIdx.x + 1) * p.total / gridDim.x;
+        if (e <= x) {
+            kx0 = 0;
+            nkx = 0;
+        } else if (x / p.num_kb == (e - 1) / p.num_kb) {
+            kx0 = static_cast<int>(x % p.num_kb);
+            nkx = static_cast<int>(e - x);
+        } else {
+            kx0 = 0;
+            nkx = p.num_kb;
+        }
+    } else {
+        kx0 = 0;
+        nkx = p.num_kb;
+    }
+}
+
+template <int MT, bool kFX = false>
 __global__ void __launch_bounds__(SK_THREADS, 1)
     fp8_gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                            const __grid_constant__ CUtensorMap tmS, const SkParams p) {
     using C = SkCfg<MT>;
     using SegIter = SegIterT<(MT <= 128)>;
-    constexpr int STAGES = C::STAGES;
+    static_assert(!kFX || MT == 16, "fused activation quantization: MT = 16 only");
+    constexpr int STAGES = kFX ? SkFxCfg::STAGES : C::STAGES;
     constexpr int NBUF = C::NBUF;
     constexpr int COLS = C::COLS;
     constexpr int SA_STRIDE = C::SA_SLOT / 4;  // floats between stages' scale slots
+    constexpr uint32_t TX_BYTES = kFX ? static_cast<uint32_t>(C::W_TILE) : static_cast<uint32_t>(C::TX_BYTES);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* smW = smem;
+    // kFX: smX = the persistent activation-code region (kFxSlots x 2 KB), smS its scales [slot][16]
     uint8_t* smX = smW + STAGES * C::W_TILE;
-    float* smS = reinterpret_cast<float*>(smX + STAGES * C::X_TILE);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smS + STAGES * SA_STRIDE);
+    float* smS = reinterpret_cast<float*>(smX + (kFX ? kFxSlots * SkFxCfg::X_SLOT : STAGES * C::X_TILE));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smS + (kFX ? kFxSlots * MT : STAGES * SA_STRIDE));
     uint64_t* empty = full + STAGES;    // the MMA consumed W and X of the stage
     uint64_t* sempty = empty + STAGES;  // the promotion warps consumed its activation scales
     uint64_t* tfull = sempty + STAGES;
     uint64_t* tempty = tfull + NBUF;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+    uint64_t* xready = tempty + NBUF;   // kFX: the activation codes and scales are in shared memory
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + 1);
+    __shared__ ScaleTables tabs;
+    int kx0 = 0, nkx = 0;
+    if (kFX) sk_fx_range(p, kx0, nkx);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -279,8 +332,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], SK_EPI_WARPS);
         }
+        mbar_init(xready, 1);
         fence_mbar_init();
     }
+    if (kFX) init_scale_tables(tabs);
     if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
     tc_fence_before();
     __syncthreads();
@@ -309,7 +364,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                 const uint32_t cap = min(static_cast<uint32_t>(STAGES), static_cast<uint32_t>(p.prefetch));
                 while (n < cap && pre.next(p, pt, pk0, pk1))
                     for (int kb = pk0; kb < pk1 && n < cap; ++kb, ++n) {
-                        mbar_arrive_expect_tx(&full[n], C::TX_BYTES);
+                        mbar_arrive_expect_tx(&full[n], TX_BYTES);
                         tma_load_2d(smW + n * C::W_TILE, &tmW, &full[n], kb * SK_BK, pt * SK_BN);
                     }
                 npf = n;
@@ -323,14 +378,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                     const bool prefetched = it < npf;  // W already in flight, expect_tx armed
                     if (!prefetched) {
                         mbar_wait(&empty[stage], ph ^ 1u);
-                        mbar_wait(&sempty[stage], ph ^ 1u);
+                        if (!kFX) mbar_wait(&sempty[stage], ph ^ 1u);
                     }
                     if (!prefetched) {
-                        mbar_arrive_expect_tx(&full[stage], C::TX_BYTES);
+                        mbar_arrive_expect_tx(&full[stage], TX_BYTES);
                         tma_load_2d(smW + stage * C::W_TILE, &tmW, &full[stage], kb * SK_BK, tile * SK_BN);
                     }
-                    tma_load_2d(smX + stage * C::X_TILE, &tmX, &full[stage], kb * SK_BK, 0);
-                    tma_load_2d(smS + stage * SA_STRIDE, &tmS, &full[stage], 0, kb);
+                    if (!kFX) {
+                        tma_load_2d(smX + stage * C::X_TILE, &tmX, &full[stage], kb * SK_BK, 0);
+                        tma_load_2d(smS + stage * SA_STRIDE, &tmS, &full[stage], 0, kb);
+                    }
                 }
             }
             FP8Q_TREC(trace_tag, 2);
@@ -346,6 +403,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             SegIter seg;
             seg.init(p);
             int tile, kb0, kb1;
+            if (kFX) mbar_wait(xready, 0);  // the CTA's activation codes are in shared memory
             while (seg.next(p, tile, kb0, kb1)) {
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
@@ -357,7 +415,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                     if (it == 0) FP8Q_TREC(trace_tag, 3);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(smW + stage * C::W_TILE);
-                    const uint32_t b0 = smem_u32(smX + stage * C::X_TILE);
+                    const uint32_t b0 = kFX ? smem_u32(smX + (kb - kx0) * SkFxCfg::X_SLOT)
+                                            : smem_u32(smX + stage * C::X_TILE);
                     const uint32_t d = tmem + buf * MT;
 #pragma unroll
                     for (int kk = 0; kk < SK_BK / 32; ++kk)
@@ -373,6 +432,52 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         // ---------------------------------------------------------------- promotion warps
         regs_inc<SK_REGS_EPI>();
         grid_dependency_wait();  // before any global write (D, workspace): the previous grid is done
+        if (kFX) {
+            // ---- fused activation quantization (the quantizers' element map, group_quant.cuh):
+            // group (token j, k-block kx0 + s) -> 128 codes at row j of slot s (SW128: 16-byte
+            // chunk c of row j at chunk position c ^ (j & 7)) and its scale at smS[s][j]; rows
+            // m..15 (the MMA's zero padding) get zero codes and scales.  One warp per group: lane
+            // l holds channels 4l..4l+3.
+            const int ew = warp - SK_EPI_WARP0;
+            const int m = p.m;
+            for (int i = ew * 32 + lane; i < nkx * (MT - m) * 8; i += SK_EPI_WARPS * 32) {
+                const int s = i / ((MT - m) * 8), rem = i - s * (MT - m) * 8;
+                const int j = m + rem / 8, c = rem % 8;
+                st_shared_v4(smem_u32(smX + s * SkFxCfg::X_SLOT + j * 128 + c * 16), 0u, 0u, 0u, 0u);
+            }
+            for (int i = ew * 32 + lane; i < nkx * MT; i += SK_EPI_WARPS * 32)
+                if (i % MT >= m) smS[i] = 0.0f;
+            uint32_t bad = 0;
+            for (int i = ew; i < m * nkx; i += SK_EPI_WARPS) {
+                const int j = i / nkx, s = i - j * nkx;
+                const uint16_t* xg = p.x + int64_t(j) * p.ld_x + int64_t(kx0 + s) * 128 + 4 * lane;
+                uint32_t w[2];
+                asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "l"(xg));
+                const uint32_t a2 = bmax_abs2(w[0], w[1]) & 0x7FFF7FFFu;
+                const uint32_t ab = __reduce_max_sync(0xFFFFFFFFu, max(a2 & 0xFFFFu, a2 >> 16));
+                const bool fast = ab >= kAmaxFastGuardBits && ab < kNonFiniteBits;  // warp-uniform
+                float sc, rc = 0.0f;
+                uint32_t code;
+                if (fast) {
+                    table_scale_rcp(tabs, ab, sc, rc);
+                    encode_words<true, 2>(w, sc, rc, &code);
+                } else {
+                    sc = scale_from_amax_bits(ab);
+                    encode_words<false, 2>(w, sc, 0.0f, &code);
+                }
+                const uint32_t chunk = static_cast<uint32_t>(lane >> 2) ^ static_cast<uint32_t>(j & 7);
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(smX + s * SkFxCfg::X_SLOT + j * 128) +
+                                                           chunk * 16u + static_cast<uint32_t>(lane & 3) * 4u),
+                             "r"(code)
+                             : "memory");
+                if (lane == 0) smS[s * MT + j] = sc;
+                bad |= ab >= kNonFiniteBits ? 1u : 0u;
+            }
+            if (bad && lane == 0 && p.flag != nullptr) *p.flag = 1;
+            fence_proxy_async_smem();  // the generic-proxy code stores, before the MMA reads them
+            asm volatile("bar.sync 1, %0;" ::"n"(SK_EPI_WARPS * 32) : "memory");
+            if (threadIdx.x == SK_EPI_WARP0 * 32) mbar_arrive(xready);
+        }
         if (threadIdx.x == SK_EPI_WARP0 * 32) FP8Q_TREC(trace_tag, 5);
         const int qd = warp & 3;                       // TMEM lane quarter of this warp
         const int h = (warp - SK_EPI_WARP0) >> 2;      // token-column half
@@ -399,9 +504,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                 const uint32_t buf = it % NBUF;
                 const uint32_t bph = (it / NBUF) & 1u;
                 mbar_wait(&tfull[buf], bph);
-                mbar_wait(&full[stage], ph);  // (already complete) orders the TMA-written scales
+                if (!kFX) mbar_wait(&full[stage], ph);  // (already complete) orders the TMA-written scales
                 tc_fence_after();
-                const float* sa_s = smS + stage * SA_STRIDE + j0;
+                const float* sa_s = kFX ? smS + (kb - kx0) * MT + j0 : smS + stage * SA_STRIDE + j0;
                 // chunks of <= 16 columns keep the live registers at acc + one chunk
                 constexpr int CH = COLS < 16 ? COLS : 16;
 #pragma unroll
@@ -426,7 +531,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sempty[stage]);  // the scales were read
+                if (!kFX && lane == 0) mbar_arrive(&sempty[stage]);  // the scales were read
             }
             const int64_t n_row = int64_t(tile) * SK_BN + r_in;
             if (p.streamk == 2) {
@@ -671,6 +776,9 @@ cudaError_t sk_device_info(int& sms) {
         SK_ATTR(128)
         SK_ATTR(256)
 #undef SK_ATTR
+        e = cudaFuncSetAttribute(fp8_gemm_skinny_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(SkFxCfg::SMEM_BYTES));
+        if (e != cudaSuccess) return e;
         di.attr_set = true;
     }
     sms = di.sms;
@@ -720,6 +828,7 @@ int sk_cluster_size(int tiles, int num_kb, int sms) {
 
 template <int MT>
 cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encode, int sms, cudaStream_t stream) {
+    const bool fx = MT == 16 && a.x_bf16 != nullptr;  // fused activation quantization
     CUtensorMap tmW, tmX, tmS;
     {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.n)};
@@ -731,7 +840,10 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    {
+    if (fx) {  // no activation / scale tensors: the kernel reads the BF16 activations itself
+        tmX = tmW;
+        tmS = tmW;
+    } else {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.k), static_cast<cuuint64_t>(a.m)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_a)};
         cuuint32_t box[2] = {SK_BK, MT};
@@ -741,7 +853,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    {
+    if (!fx) {
         // activation scales, MN-major [k/128][ld_sa]: row kb holds the m tokens' scales
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.m), static_cast<cuuint64_t>(a.k / SK_BK)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld_sa * 4)};
@@ -776,6 +888,9 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
         return e ? std::atoi(e) : 4;
     }();
     p.prefetch = prefetch;
+    p.x = fx ? a.x_bf16 : nullptr;
+    p.ld_x = a.ld_x;
+    p.flag = a.nonfinite_flag;
     p.ws = nullptr;
     p.counters = nullptr;
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(p.tiles, sms));  // whole tiles
@@ -802,7 +917,7 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(SK_THREADS);
-    cfg.dynamicSmemBytes = SkCfg<MT>::SMEM_BYTES;
+    cfg.dynamicSmemBytes = fx ? SkFxCfg::SMEM_BYTES : SkCfg<MT>::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     static const int no_pdl = [] {  // dev A/B: FP8Q_SKINNY_NOPDL=1 launches without PDL
@@ -817,6 +932,9 @@ cudaError_t sk_launch(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 encod
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
+    if constexpr (MT == 16) {
+        if (fx) return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<16, true>, tmW, tmX, tmS, p);
+    }
     return cudaLaunchKernelEx(&cfg, fp8_gemm_skinny_kernel<MT>, tmW, tmX, tmS, p);
 }
 
@@ -841,6 +959,22 @@ bool skinny_gemm_applies(const GemmArgs& a) {
         return sk_cluster_size<256>(static_cast<int>((a.n + SK_BN - 1) / SK_BN), static_cast<int>(a.k / SK_BK), sms) >= 2;
     }
     return forced == 16 || a.m <= 32 || (a.n + 255) / 256 < 64;
+}
+
+bool skinny_fused_act_applies(const GemmArgs& a) {
+    static const bool enabled = [] {  // dev A/B: FP8Q_LINEAR_FUSED=0 keeps quantizer + GEMM launches
+        const char* e = std::getenv("FP8Q_LINEAR_FUSED");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    if (!enabled || a.m < 1 || a.m > 16 || a.k % SK_BK != 0 || !skinny_gemm_applies(a)) return false;
+    int sms = 0;
+    if (sk_device_info(sms) != cudaSuccess) return false;
+    const int tiles = static_cast<int>((a.n + SK_BN - 1) / SK_BN);
+    const int num_kb = static_cast<int>(a.k / SK_BK);
+    const int cs = sk_cluster_size<16>(tiles, num_kb, sms);
+    // the CTA's activation k-blocks must fit the kFxSlots code slots (sk_fx_range)
+    if (cs >= 2) return (num_kb + cs - 1) / cs <= kFxSlots;
+    return num_kb <= kFxSlots;
 }
 
 size_t skinny_workspace_bytes(int64_t m, int64_t n, int64_t k) {

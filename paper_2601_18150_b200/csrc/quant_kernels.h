@@ -68,7 +68,14 @@ struct GemmArgs {
     int32_t groups;
     void* workspace;         // split-K workspace (zero-filled before first use), may be null
     size_t workspace_bytes;
+    // fp8_linear_dynamic at m <= 16 (decode): BF16 activations quantized inside the GEMM (a, sa unused)
+    const uint16_t* x_bf16 = nullptr;
+    int64_t ld_x = 0;
+    int32_t* nonfinite_flag = nullptr;
 };
+// whether the decode kernel can quantize this linear's activations itself (m <= 16, the CTA's
+// k-blocks' codes fit its shared memory); the caller then sets x_bf16 / ld_x
+bool skinny_fused_act_applies(const GemmArgs& a);
 
 // Decode-sized dense GEMMs (1 <= m <= kSkinnyMaxM) run the swap-AB kernel of gemm_skinny.cu
 // (m > 128 only where its cluster split-K mode applies).

@@ -10,6 +10,7 @@
 //   mode 4: mode 0, but the 4 MMAs of a k-block read 4 different 32-byte K slices of a
 //           stage ring of 4 stages (descriptor address moves like the real kernel)
 //   mode 5: cta_group::1 (no pair), M=128 N=256, 2 commits per k-block (each CTA issues)
+//   modes 6 / 7 / 8: as mode 5 with N = 16 / 64 / 128 (the decode kernel's swap-AB shapes)
 #include <cstdint>
 
 #include "ptx.cuh"
@@ -50,7 +51,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     cluster_sync_all();
-    const bool pair = mode != 5;
+    const bool pair = mode < 5;
     if (warp == 1) {
         if (pair)
             tmem_alloc_pair(slot, 512);
@@ -63,7 +64,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(slot);
     const bool issuer = threadIdx.x == 0 && (rank == 0 || !pair);
     if (issuer) {
-        const uint32_t N = mode == 3 ? 128 : 256;
+        const uint32_t N = mode == 3 ? 128 : mode == 6 ? 16 : mode == 7 ? 64 : mode == 8 ? 128 : 256;
         const uint32_t idesc = pair ? idesc_e4m3_f32(256, N) : idesc_e4m3_f32(128, N);
         const long long t0 = clock64();
         for (int kb = 0; kb < nkb; ++kb) {
@@ -84,7 +85,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
                 mma_commit_pair(&bars[4 + (kb & 1)], 0x3);
             } else if (mode == 2) {
                 mma_commit_pair(&bars[kb & 3], 0x3);
-            } else if (mode == 5) {
+            } else if (mode >= 5) {
                 commit_1(&bars[kb & 3]);
                 commit_1(&bars[4 + (kb & 1)]);
             }
