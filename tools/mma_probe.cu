@@ -11,6 +11,8 @@
 //           stage ring of 4 stages (descriptor address moves like the real kernel)
 //   mode 5: cta_group::1 (no pair), M=128 N=256, 2 commits per k-block (each CTA issues)
 //   modes 6 / 7 / 8: as mode 5 with N = 16 / 64 / 128 (the decode kernel's swap-AB shapes)
+//   mode 9: mode 6 plus the decode issuer's per-k-block bookkeeping: two mbarrier waits on
+//           (already completed) barriers and a tcgen05 fence before the MMAs
 #include <cstdint>
 
 #include "ptx.cuh"
@@ -46,6 +48,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     for (int i = threadIdx.x; i < 8 * 16384 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x38383838u;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 9; ++i) mbar_init(&bars[i], 1);
+        mbar_init(&bars[12], 1);
+        mbar_init(&bars[13], 1);
+        mbar_arrive(&bars[12]);
+        mbar_arrive(&bars[13]);
         fence_mbar_init();
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -64,13 +70,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(slot);
     const bool issuer = threadIdx.x == 0 && (rank == 0 || !pair);
     if (issuer) {
-        const uint32_t N = mode == 3 ? 128 : mode == 6 ? 16 : mode == 7 ? 64 : mode == 8 ? 128 : 256;
+        const uint32_t N = mode == 3 ? 128 : (mode == 6 || mode == 9) ? 16 : mode == 7 ? 64 : mode == 8 ? 128 : 256;
         const uint32_t idesc = pair ? idesc_e4m3_f32(256, N) : idesc_e4m3_f32(128, N);
         const long long t0 = clock64();
         for (int kb = 0; kb < nkb; ++kb) {
             const uint32_t st = mode == 4 ? static_cast<uint32_t>(kb & 3) : 0u;
             const uint32_t a0 = smem_u32(smA + st * 16384), b0 = smem_u32(smB + st * 16384);
             const uint32_t d = tmem + static_cast<uint32_t>(kb & 1) * N;
+            if (mode == 9) {
+                mbar_wait(&bars[12], 0);  // completed at init: the waits return at once
+                mbar_wait(&bars[13], 0);
+                tc_fence_after();
+            }
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
                 if (pair)
