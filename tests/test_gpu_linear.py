@@ -1,6 +1,7 @@
 """fp8_linear_dynamic: one W8A8 linear with the activations quantized
-dynamically inside the call (the quantizer and the GEMM chained by programmatic dependent
-launch, the codes in the caller's workspace).  Bar: BIT-identical to the separate
+dynamically inside the call (at m <= 16 by the decode GEMM itself, in shared memory; otherwise
+the quantizer and the GEMM chained by programmatic dependent launch, the codes in the caller's
+workspace).  Bar: BIT-identical to the separate
 quantize_act_per_token_group + fp8_block_gemm calls (which the other suites pin to the oracle);
 plus a direct oracle check (oracle quantizer, fp64 GEMM) on the outputs."""
 import numpy as np
@@ -29,6 +30,28 @@ def test_linear_dynamic_equals_two_step(m, n, k):
     x = to_dev_bf16(xb)
     for dt in (torch.float32, torch.bfloat16):
         y = fp8q.fp8_linear_dynamic(x, wq, ws, out_dtype=dt)
+        xq, xs = fp8q.quantize_act_per_token_group(x)
+        ref = fp8q.fp8_block_gemm(xq, xs, wq, ws, out_dtype=dt)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int16 if dt == torch.bfloat16 else torch.int32),
+                           ref.view(torch.int16 if dt == torch.bfloat16 else torch.int32)), (m, n, k, dt)
+
+
+@pytest.mark.parametrize("m", [1, 7, 16])
+@pytest.mark.parametrize("n,k,launches", [(24576, 4096, 1), (4096, 4096, 1), (256, 16384, 1), (3072, 2048, 1),
+                                          (24576, 8192, 2)])
+def test_linear_dynamic_fused_decode_modes(m, n, k, launches):
+    # m <= 16: the decode GEMM quantizes its own activations where its CTAs' k-blocks fit the
+    # shared-memory slots -- ordered stream-K whose ranges cross tiles (gate_up: every k-block),
+    # cluster split-K (o_proj: cs = 4; 2 tiles of K = 16384: cs = 8, 16 k-blocks per CTA) -- and
+    # falls back to two launches where they do not (stream-K over 64 k-blocks); every mode
+    # bit-identical to the separate calls
+    _, wq, ws = _weight(n, k, 13)
+    x = to_dev_bf16(synth.qwen3_activation(m, k, seed=3 * m + 1))
+    for dt in (torch.float32, torch.bfloat16):
+        before = fp8q.kernel_launches()
+        y = fp8q.fp8_linear_dynamic(x, wq, ws, out_dtype=dt)
+        assert fp8q.kernel_launches() - before == launches, (m, n, k)
         xq, xs = fp8q.quantize_act_per_token_group(x)
         ref = fp8q.fp8_block_gemm(xq, xs, wq, ws, out_dtype=dt)
         torch.cuda.synchronize()
