@@ -448,30 +448,45 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             for (int i = ew * 32 + lane; i < nkx * MT; i += SK_EPI_WARPS * 32)
                 if (i % MT >= m) smS[i] = 0.0f;
             uint32_t bad = 0;
-            for (int i = ew; i < m * nkx; i += SK_EPI_WARPS) {
-                const int j = i / nkx, s = i - j * nkx;
-                const uint16_t* xg = p.x + int64_t(j) * p.ld_x + int64_t(kx0 + s) * 128 + 4 * lane;
-                uint32_t w[2];
-                asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "l"(xg));
-                const uint32_t a2 = bmax_abs2(w[0], w[1]) & 0x7FFF7FFFu;
-                const uint32_t ab = __reduce_max_sync(0xFFFFFFFFu, max(a2 & 0xFFFFu, a2 >> 16));
-                const bool fast = ab >= kAmaxFastGuardBits && ab < kNonFiniteBits;  // warp-uniform
-                float sc, rc = 0.0f;
-                uint32_t code;
-                if (fast) {
-                    table_scale_rcp(tabs, ab, sc, rc);
-                    encode_words<true, 2>(w, sc, rc, &code);
-                } else {
-                    sc = scale_from_amax_bits(ab);
-                    encode_words<false, 2>(w, sc, 0.0f, &code);
+            // groups in batches of 4 per warp, the batch's loads issued before any is used (the
+            // activations may come from DRAM: one round trip per batch, not per group)
+            for (int i0 = ew; i0 < m * nkx; i0 += 4 * SK_EPI_WARPS) {
+                uint32_t w[4][2];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int i = i0 + b * SK_EPI_WARPS;
+                    w[b][0] = w[b][1] = 0u;
+                    if (i < m * nkx) {
+                        const int j = i / nkx, s = i - j * nkx;
+                        const uint16_t* xg = p.x + int64_t(j) * p.ld_x + int64_t(kx0 + s) * 128 + 4 * lane;
+                        asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(w[b][0]), "=r"(w[b][1]) : "l"(xg));
+                    }
                 }
-                const uint32_t chunk = static_cast<uint32_t>(lane >> 2) ^ static_cast<uint32_t>(j & 7);
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(smX + s * SkFxCfg::X_SLOT + j * 128) +
-                                                           chunk * 16u + static_cast<uint32_t>(lane & 3) * 4u),
-                             "r"(code)
-                             : "memory");
-                if (lane == 0) smS[s * MT + j] = sc;
-                bad |= ab >= kNonFiniteBits ? 1u : 0u;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int i = i0 + b * SK_EPI_WARPS;
+                    if (i >= m * nkx) break;  // warp-uniform
+                    const int j = i / nkx, s = i - j * nkx;
+                    const uint32_t a2 = bmax_abs2(w[b][0], w[b][1]) & 0x7FFF7FFFu;
+                    const uint32_t ab = __reduce_max_sync(0xFFFFFFFFu, max(a2 & 0xFFFFu, a2 >> 16));
+                    const bool fast = ab >= kAmaxFastGuardBits && ab < kNonFiniteBits;  // warp-uniform
+                    float sc, rc = 0.0f;
+                    uint32_t code;
+                    if (fast) {
+                        table_scale_rcp(tabs, ab, sc, rc);
+                        encode_words<true, 2>(w[b], sc, rc, &code);
+                    } else {
+                        sc = scale_from_amax_bits(ab);
+                        encode_words<false, 2>(w[b], sc, 0.0f, &code);
+                    }
+                    const uint32_t chunk = static_cast<uint32_t>(lane >> 2) ^ static_cast<uint32_t>(j & 7);
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(smX + s * SkFxCfg::X_SLOT + j * 128) +
+                                                               chunk * 16u + static_cast<uint32_t>(lane & 3) * 4u),
+                                 "r"(code)
+                                 : "memory");
+                    if (lane == 0) smS[s * MT + j] = sc;
+                    bad |= ab >= kNonFiniteBits ? 1u : 0u;
+                }
             }
             if (bad && lane == 0 && p.flag != nullptr) *p.flag = 1;
             fence_proxy_async_smem();  // the generic-proxy code stores, before the MMA reads them
