@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         // the peers' shared memory through DSMEM, and stores them.  No global workspace, no
         // fences, no atomics.
         cluster_sync_all();
-        if (warp >= SK_EPI_WARP0) {  // the promotion warps (216 registers; warps 0-3 hold 72)
+        {  // all 12 warps (the control warps' 72 registers hold one unit's cs loads)
             grid_dependency_wait();
             const uint32_t rank = cluster_ctarank();
             const int tile = static_cast<int>(blockIdx.x) / p.cs;
@@ -689,13 +689,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             const int U = p.m * (SK_BN / 4);
             const int u1 = static_cast<int>((int64_t(rank) + 1) * U / p.cs);
             const uint32_t red0 = smem_u32(smW);
-            const int te = threadIdx.x - SK_EPI_WARP0 * 32;
+            const int te = threadIdx.x;
             constexpr int RU = 1;  // units per thread per pass (all cs loads of a unit in flight together)
-            for (int q0 = static_cast<int>(int64_t(rank) * U / p.cs) + te; q0 < u1; q0 += RU * SK_EPI_WARPS * 32) {
+            for (int q0 = static_cast<int>(int64_t(rank) * U / p.cs) + te; q0 < u1; q0 += RU * SK_THREADS) {
                 float4 v[RU][8];
 #pragma unroll
                 for (int r = 0; r < RU; ++r) {
-                    const int q = q0 + r * SK_EPI_WARPS * 32;
+                    const int q = q0 + r * SK_THREADS;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
                         if (c < p.cs && q < u1) {
@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                 }
 #pragma unroll
                 for (int r = 0; r < RU; ++r) {
-                    const int q = q0 + r * SK_EPI_WARPS * 32;
+                    const int q = q0 + r * SK_THREADS;
                     if (q >= u1) break;
                     float4 sum = v[r][0];
 #pragma unroll
