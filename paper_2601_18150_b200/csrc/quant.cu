@@ -526,12 +526,15 @@ __device__ __forceinline__ void tma_load_3d_hint(void* smem_dst, const void* des
         "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
+// kMasked = false: the slot's groups past the row are zeros already (the TMA box's zero fill),
+// so every lane loads unconditionally.
+template <bool kMasked>
 __device__ __forceinline__ void aq_load_smem(uint32_t base, int64_t groups, int64_t chunk, AItemRegs& d) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int64_t g = chunk * 16 + 4 * j + (lane >> 3);
-        if (g < groups) {
+        if (!kMasked || g < groups) {
             const uint32_t a = base + static_cast<uint32_t>((4 * j + (lane >> 3)) * 256 + (lane & 7) * 32);
             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(d.v[j][0]), "=r"(d.v[j][1]), "=r"(d.v[j][2]), "=r"(d.v[j][3]) : "r"(a));
@@ -650,7 +653,7 @@ __global__ void __launch_bounds__(ABQ_THREADS, 1) act_per_token_group_bulk_kerne
             const uint32_t chunk = md.y & 0xFFFFu;
             const uint32_t groups = static_cast<uint32_t>(t.groups);
             AItemRegs d;
-            aq_load_smem(ring + (s * ABQ_ITEMS + w) * ABQ_ITEM_BYTES, groups, chunk, d);
+            aq_load_smem<!kTma>(ring + (s * ABQ_ITEMS + w) * ABQ_ITEM_BYTES, groups, chunk, d);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // the row is in registers: free the slot
             aq_process_item(d, t.q + int64_t(row) * t.ld_q, t.scales + row, static_cast<uint32_t>(t.ld_s), groups,
