@@ -235,7 +235,7 @@ LAYER = [("qkv",) + synth.QWEN3_8B_LINEARS["qkv"], ("o",) + synth.QWEN3_8B_LINEA
 E2E_ORDER = [LAYER[2], LAYER[3], LAYER[1], LAYER[0]]  # gate_up, down, o, qkv
 # activation upload / GEMM / read-back row blocks per GEMM (the same PCIe model: 19.0 -> 17.0 ms
 # at 4 blocks; the GEMMs run on 2,048-row blocks, hidden behind the transfers)
-E2E_CHUNKS = 4
+E2E_CHUNKS = int(os.environ.get("FP8Q_E2E_CHUNKS", "4"))  # row blocks per GEMM in the e2e pipeline (env: dev A/B)
 
 
 def layer_flops(m):
