@@ -206,9 +206,11 @@ fp8q_status silu_mul_quantize_act_per_token_group(const void* gate_up_bf16, int6
  *           fp8_block_gemm_workspace_size(m, n, k) bytes (256-byte aligned, ZERO-FILLED before
  *           its first use; every launch leaves it zeroed again), small-M problems (decode,
  *           M <= 128) whose weight has many 128-row tiles split the K loop over more CTAs
- *           (stream-K): slices park fp32 partials in the workspace and the last slice of each
- *           tile sums them in slice order (deterministic).  Without it the same problem runs
- *           unsplit (slower, equally correct).  A workspace must not be shared by concurrently
+ *           (stream-K), and the tile kernels split the K loop of the tiles of their last,
+ *           partial wave (the "tail": T mod U tiles, U = SMs or CTA pairs) into slices:
+ *           slices park fp32 partials in the workspace and the last slice of each tile sums
+ *           them in slice order (deterministic).  Without it the same problem runs unsplit
+ *           (slower, equal up to fp32 summation order).  A workspace must not be shared by concurrently
  *           running GEMMs.  Weights with few tiles (tiles <= SMs / 2) split K inside a thread-
  *           block cluster instead (partials reduced in CTA-rank order through distributed
  *           shared memory) and never touch the workspace.

@@ -99,6 +99,8 @@ struct KParams {
     float* ws;               // split-K partials [tile][split][128][BN] fp32
     int32_t* counters;       // split-K arrival counters [tile], zero between launches
     int groups;
+    int dp_tiles;            // tiles [0, dp_tiles) whole, the rest in `splits` K slices
+    int fix_bulk;            // split fixup through the idle smem ring (each CTA's last item only)
 };
 
 // Walks the (group, m-tile, n-tile) sequence; t must increase between calls.  TM = rows per
@@ -185,8 +187,9 @@ struct EpiTile {
     int64_t col0;     // first of this thread's columns
     int g;            // group (MoE expert) index
     int kb0, kb1;     // this work item's k-block range
-    int64_t tile;     // linear tile index (split-K bookkeeping)
+    int tile;         // split-K workspace tile index (pair: local split tile * 2 + CTA rank)
     int split;        // split-K slice of this work item
+    int nsplit;       // K slices of this tile (1: whole tile, stored directly)
 };
 // The first two k-blocks' (sa, sb) of a tile: loaded one tile ahead so the HBM/L2 latency of
 // the first scales overlaps the previous tile's last k-blocks and stores.
@@ -234,11 +237,30 @@ __device__ __forceinline__ int split_begin(const KParams& p, int s) {
     return (s * p.num_kb) / p.splits;  // 32-bit: s * num_kb < 2^31 for any real K
 }
 
+// Work item v (split plans: plan_split): below dp_tiles the whole tile v;
+// past it slice sp of tile dp_tiles + (v - dp_tiles) / splits.  Returns the tile index (past
+// the last tile when v is), its k-block range in [kb0, kb1).
+__device__ __forceinline__ int work_item(const KParams& p, int v, int& sp, int& kb0, int& kb1) {
+    if (v < p.dp_tiles) {
+        sp = 0;
+        kb0 = 0;
+        kb1 = p.num_kb;
+        return v;
+    }
+    const int u = v - p.dp_tiles;
+    const int tq = u / p.splits;
+    sp = u - tq * p.splits;
+    kb0 = split_begin(p, sp);
+    kb1 = split_begin(p, sp + 1);
+    return p.dp_tiles + tq;
+}
+
 // For every k-block: wait for the partial in TMEM buffer it % NBUF, tcgen05.ld it, hand the
 // buffer back (to the leader CTA of a pair when PAIR), and
 // acc += P_kb * (sa[kb][row] * sb[col0/128][kb]) with packed FFMA2; then store the tile.
 template <int BN, int NBUF, bool PAIR>
 __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap* tmD, uint8_t* stg,
+                                             uint8_t* ring, uint64_t* fixbar,
                                              const EpiTile& tile, const ScalePre& pre, bool has_next,
                                              const EpiTile& next, ScalePre& next_pre, uint32_t tmem,
                                              int qd, int h, int lane, uint64_t* tfull,
@@ -300,16 +322,21 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
             }
         }
     }
-    if (!PAIR && p.splits > 1) {
+    if (tile.nsplit > 1) {
         // ---- split-K: park this slice's fp32 partial; the last slice to arrive sums all
-        // slices in slice order (deterministic) and stores the tile.
+        // slices in slice order (deterministic) and stores the tile.  Layout per (tile, slice):
+        // [column half h][16-byte unit j][row] -- a warp's access to unit j covers its 32
+        // consecutive rows, 512 contiguous bytes.  (Row-major partials, each lane 1 KB from the
+        // next, made the fixup ~4x slower than the k-loop it split: 32 sectors per instruction.)
         __shared__ int sk_last;
-        const int r_in = qd * 32 + lane;  // row within the tile
-        float* mine = p.ws + ((tile.tile * p.splits + tile.split) * BM + r_in) * BN + h * EPI_COLS;
+        constexpr int UNITS = EPI_COLS / 4;  // 16-byte units per thread
+        const int r_in = qd * 32 + lane;     // row within the tile
+        float4* mine = reinterpret_cast<float4*>(p.ws) +
+                       ((tile.tile * tile.nsplit + tile.split) * 2 + h) * UNITS * BM + r_in;
         if (live) {  // only real rows/columns are parked and summed (decode: M << 128)
 #pragma unroll
-            for (int j = 0; j < EPI_COLS / 4; ++j)
-                st_v4(mine + 4 * j, __float_as_uint(acc[2 * j].x), __float_as_uint(acc[2 * j].y),
+            for (int j = 0; j < UNITS; ++j)
+                st_v4(mine + j * BM, __float_as_uint(acc[2 * j].x), __float_as_uint(acc[2 * j].y),
                       __float_as_uint(acc[2 * j + 1].x), __float_as_uint(acc[2 * j + 1].y));
         }
         __threadfence();
@@ -317,18 +344,54 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
         if (threadIdx.x == EPI_WARP0 * 32) {
             const int old = atomicAdd(&p.counters[tile.tile], 1);
             __threadfence();
-            sk_last = (old == p.splits - 1);
+            sk_last = (old == tile.nsplit - 1);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
         if (!sk_last) return;
-        const float* base = p.ws + (tile.tile * p.splits * BM + r_in) * BN + h * EPI_COLS;
+        if (p.fix_bulk) {
+            // This slice was the CTA's last work item and its MMAs have completed, so the
+            // shared-memory ring is idle: bulk-copy each slice's 64 KB column half into it (one
+            // copy in flight per half, issued by the half's first warp) and add from shared
+            // memory -- the register path below keeps only ~16 loads per thread in flight and
+            // is bound by L2 latency.
+            constexpr uint32_t HALF_BYTES = UNITS * BM * 16;
+            uint8_t* buf = ring + h * HALF_BYTES;
+            const float4* src = reinterpret_cast<const float4*>(p.ws) + (tile.tile * tile.nsplit * 2 + h) * UNITS * BM;
+            const bool issuer = qd == 0 && lane == 0;
+            if (issuer) fence_proxy_async_global();
+#pragma unroll
+            for (int j = 0; j < EPI_COLS / 2; ++j) acc[j] = make_float2(0.f, 0.f);
+            for (int sl = 0; sl < tile.nsplit; ++sl) {
+                if (issuer) {
+                    mbar_arrive_expect_tx(&fixbar[h], HALF_BYTES);
+                    bulk_load_g2s(smem_u32(buf), src + sl * 2 * UNITS * BM, HALF_BYTES, &fixbar[h]);
+                }
+                mbar_wait(&fixbar[h], static_cast<uint32_t>(sl) & 1u);
+                const uint32_t rb = smem_u32(buf) + static_cast<uint32_t>(r_in) * 16u;
+#pragma unroll
+                for (int j = 0; j < UNITS; ++j) {
+                    uint32_t x0, x1, x2, x3;
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                                 : "r"(rb + static_cast<uint32_t>(j * BM) * 16u));
+                    acc[2 * j].x += __uint_as_float(x0);
+                    acc[2 * j].y += __uint_as_float(x1);
+                    acc[2 * j + 1].x += __uint_as_float(x2);
+                    acc[2 * j + 1].y += __uint_as_float(x3);
+                }
+                // the half's 4 warps are done with buf before the next slice overwrites it
+                asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory");
+            }
+            if (threadIdx.x == EPI_WARP0 * 32) p.counters[tile.tile] = 0;  // reusable workspace
+        } else {
+        const float4* base = reinterpret_cast<const float4*>(p.ws) + (tile.tile * tile.nsplit * 2 + h) * UNITS * BM + r_in;
 #pragma unroll
         for (int j = 0; j < EPI_COLS / 2; ++j) acc[j] = make_float2(0.f, 0.f);
-        for (int sl = 0; sl < p.splits && live; ++sl) {
-            const float4* src = reinterpret_cast<const float4*>(base + int64_t(sl) * BM * BN);
+        for (int sl = 0; sl < tile.nsplit && live; ++sl) {
+            const float4* src = base + sl * 2 * UNITS * BM;
 #pragma unroll
-            for (int j = 0; j < EPI_COLS / 4; ++j) {
-                const float4 v = __ldcg(src + j);
+            for (int j = 0; j < UNITS; ++j) {
+                const float4 v = __ldcg(src + j * BM);
                 acc[2 * j].x += v.x;
                 acc[2 * j].y += v.y;
                 acc[2 * j + 1].x += v.z;
@@ -336,6 +399,7 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
             }
         }
         if (threadIdx.x == EPI_WARP0 * 32) p.counters[tile.tile] = 0;  // reusable workspace
+        }
     }
     if (col0 >= p.n) return;  // warp-uniform: these columns are past the matrix
     // ---- output: the warp's 32 rows x EPI_COLS columns, through the warp's smem staging:
@@ -345,7 +409,7 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
     // also covers MoE group tails).  Plain loads/stores: no async-proxy fence, no TMA queue.
     (void)tmD;
     const int64_t row_base = row - lane;
-    if (!p.out_f32 && p.splits == 1 && EPI_COLS * 2 == 4 * 64) {  // must match the store-warp role
+    if (!p.out_f32 && tile.nsplit == 1 && EPI_COLS * 2 == 4 * 64) {  // must match the store-warp role
         // BF16 production path: park the row segment in this warp's staging (64-byte swizzled
         // 16 B units, conflict-free) and hand it to the store warp of this column half, which
         // writes it to global memory while this warp already promotes the next tile.
@@ -373,6 +437,9 @@ __device__ __forceinline__ void promote_tile(const KParams& p, const CUtensorMap
         if (lane == 0) mbar_arrive(&stg_full[h]);  // release: the staging writes above
         return;
     }
+    // a split tile after whole ones: the store warp may still be draining this
+    // warp's staging from the last parked tile
+    if (tile_no > 0) mbar_wait(&stg_empty[h], (tile_no - 1) & 1u);
     const uint32_t swz = static_cast<uint32_t>((lane >> 1) & 3);
     const uint32_t stg_base = smem_u32(stg);
     // One staging pass: CH chunks of 32 rows x 64 B (CH = 4 -> 256 B row segments, 16 lanes
@@ -496,7 +563,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint64_t* tempty = tfull + NBUF;
     uint64_t* stg_full = tempty + NBUF;   // [2]: per column half, 4 promotion warps arrive
     uint64_t* stg_empty = stg_full + 2;   // [2]: the store warp of that half arrives
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + 2);
+    uint64_t* fixbar = stg_empty + 2;     // [2]: split fixup bulk loads, per column half
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixbar + 2);
     // MoE: the group offsets in shared memory -- every role's tile cursor walks them at every
     // tile, and from global memory each step of that walk is a dependent L2 round trip
     __shared__ int32_t s_offs[kSmemGroups + 1];
@@ -520,6 +588,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int hh = 0; hh < 2; ++hh) {
             mbar_init(&stg_full[hh], 4);
             mbar_init(&stg_empty[hh], 1);
+            mbar_init(&fixbar[hh], 1);
         }
         fence_mbar_init();
     }
@@ -539,13 +608,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             cur.init(p, offs);
             uint32_t it = 0;
             int mt, nt;
-            for (int item = blockIdx.x;; item += gridDim.x) {
-                const int tq = item / p.splits;
-                if (!cur.seek(p, tq, mt, nt)) break;
-                const int sp = item - tq * p.splits;
+            // whole tiles, then split slices (work_item); one body instance per form keeps the
+            // whole-tile loop's k range in the constant bank (72 registers here)
+            auto load_tile = [&](int kb0, int kb1) {
                 const int32_t arow = static_cast<int32_t>(cur.row0 + int64_t(mt) * BM);
                 const int32_t brow = nt * BN;
-                for (int kb = split_begin(p, sp); kb < split_begin(p, sp + 1); ++kb, ++it) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
                     mbar_wait(&empty[stage], ph ^ 1u);
@@ -553,7 +621,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tma_load_2d(smA + stage * A_TILE, &tmA, &full[stage], kb * BK, arow);
                     tma_load_3d(smB + stage * C::B_TILE, &tmB, &full[stage], kb * BK, brow, cur.g);
                 }
-            }
+            };
+            int v = blockIdx.x;
+            for (; v < p.dp_tiles && cur.seek(p, v, mt, nt); v += gridDim.x) load_tile(0, p.num_kb);
+            int sp, kb0, kb1;
+            for (; cur.seek(p, work_item(p, v, sp, kb0, kb1), mt, nt); v += gridDim.x) load_tile(kb0, kb1);
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -563,11 +635,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             cur.init(p, offs);
             uint32_t it = 0;
             int mt, nt;
-            for (int item = blockIdx.x;; item += gridDim.x) {
-                const int tq = item / p.splits;
-                if (!cur.seek(p, tq, mt, nt)) break;
-                const int sp = item - tq * p.splits;
-                for (int kb = split_begin(p, sp); kb < split_begin(p, sp + 1); ++kb, ++it) {
+            auto mma_tile = [&](int kb0, int kb1) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
                     const uint32_t buf = it % NBUF;
@@ -585,16 +654,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     mma_commit(&empty[stage]);
                     mma_commit(&tfull[buf]);
                 }
-            }
+            };
+            int v = blockIdx.x;
+            for (; v < p.dp_tiles && cur.seek(p, v, mt, nt); v += gridDim.x) mma_tile(0, p.num_kb);
+            int sp, kb0, kb1;
+            for (; cur.seek(p, work_item(p, v, sp, kb0, kb1), mt, nt); v += gridDim.x) mma_tile(kb0, kb1);
         }
-    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128) {
+    } else if ((warp == 2 || warp == 3) && !p.out_f32 && EPI_COLS == 128) {
         // ------------------------------------------------------------ store warps (BF16)
+        // (whole tiles only; split tiles are stored by the promotion warps)
         const int h = warp - 2;
         TileCursor<BM, RASTER_GM> cur;
         cur.init(p, offs);
         uint32_t tile_no = 0;
         int mt, nt;
-        for (int t = blockIdx.x; cur.seek(p, t, mt, nt); t += gridDim.x) {
+        for (int t = blockIdx.x; t < p.dp_tiles && cur.seek(p, t, mt, nt); t += gridDim.x) {
             const int64_t col0 = int64_t(nt) * BN + h * EPI_COLS;
             if (col0 >= p.n) {  // the promotion warps skip such halves too
                 continue;
@@ -615,24 +689,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         cur.init(p, offs);
         uint32_t it = 0;
         uint32_t tile_no = 0;
-        auto make_tile = [&](int item, int mt, int nt) {
-            const int tq = item / p.splits;
-            const int sp = item - tq * p.splits;
+        int sp = 0, kb0 = 0, kb1 = 0;
+        auto make_tile = [&](int tq, int mt, int nt) {
+            const bool split = tq >= p.dp_tiles;
             return EpiTile{cur.row0 + int64_t(mt) * BM + r_in_tile, int64_t(cur.row0) + cur.rows,
-                           int64_t(nt) * BN + h * EPI_COLS, cur.g, split_begin(p, sp), split_begin(p, sp + 1),
-                           tq, sp};
+                           int64_t(nt) * BN + h * EPI_COLS, cur.g, kb0, kb1, split ? tq - p.dp_tiles : 0, sp,
+                           split ? p.splits : 1};
         };
         int mt = 0, nt = 0;
-        int t = blockIdx.x;  // work item = tile * splits + split
-        bool have = cur.seek(p, t / p.splits, mt, nt);
-        EpiTile tile = have ? make_tile(t, mt, nt) : EpiTile{0, 0, 0, 0, 0, 0, 0, 0};
+        int t = blockIdx.x;  // work item (work_item)
+        int tq = work_item(p, t, sp, kb0, kb1);
+        bool have = cur.seek(p, tq, mt, nt);
+        EpiTile tile = have ? make_tile(tq, mt, nt) : EpiTile{0, 0, 0, 0, 0, 0, 0, 0, 1};
         ScalePre pre = prefetch_scales(p, tile);
         while (have) {
             const int tn = t + gridDim.x;
-            const bool have_next = cur.seek(p, tn / p.splits, mt, nt);
-            const EpiTile next = have_next ? make_tile(tn, mt, nt) : tile;
+            tq = work_item(p, tn, sp, kb0, kb1);
+            const bool have_next = cur.seek(p, tq, mt, nt);
+            const EpiTile next = have_next ? make_tile(tq, mt, nt) : tile;
             ScalePre next_pre = pre;
-            promote_tile<BN, NBUF, false>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd, h,
+            promote_tile<BN, NBUF, false>(p, &tmD, stg, smem, fixbar, tile, pre, have_next, next, next_pre, tmem, qd, h,
                                           lane, tfull, tempty, it, stg_full, stg_empty, tile_no);
             tile = next;
             pre = next_pre;
@@ -700,7 +776,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint64_t* tempty = tfull + NBUF;
     uint64_t* stg_full = tempty + NBUF;
     uint64_t* stg_empty = stg_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_empty + 2);
+    uint64_t* fixbar = stg_empty + 2;     // [2]: split fixup bulk loads, per column half
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixbar + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -723,6 +800,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int hh = 0; hh < 2; ++hh) {
             mbar_init(&stg_full[hh], 4);
             mbar_init(&stg_empty[hh], 1);
+            mbar_init(&fixbar[hh], 1);
         }
         fence_mbar_init();
     }
@@ -743,10 +821,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
-            for (int t = static_cast<int>(pair); cur.seek(p, t, mt, nt); t += static_cast<int>(npairs)) {
+            // whole tiles, then at most one tail-wave slice (pair_item); one body instance per
+            // form keeps the whole-tile loop's k range in the constant bank (72 registers here)
+            auto load_tile = [&](int kb0, int kb1) {
                 const int32_t arow = static_cast<int32_t>(cur.row0 + int64_t(mt) * 2 * BM + rank * BM);
                 const int32_t brow = nt * PAIR_BN + static_cast<int32_t>(rank) * PAIR_B_HALF;
-                for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
                     mbar_wait(&empty[stage], ph ^ 1u);
@@ -757,7 +837,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     tma_load_2d_pair(smA + stage * A_TILE, &tmA, &full[stage], kb * BK, arow);
                     tma_load_3d_pair(smB + stage * (PAIR_B_HALF * BK), &tmB, &full[stage], kb * BK, brow, cur.g);
                 }
-            }
+            };
+            int v = static_cast<int>(pair);
+            for (; v < p.dp_tiles && cur.seek(p, v, mt, nt); v += static_cast<int>(npairs)) load_tile(0, p.num_kb);
+            int sp, kb0, kb1;
+            for (; cur.seek(p, work_item(p, v, sp, kb0, kb1), mt, nt); v += static_cast<int>(npairs))
+                load_tile(kb0, kb1);
         }
     } else if (warp == 1) {
         if (lane == 0 && leader) {
@@ -767,8 +852,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             cur.init(p);
             uint32_t it = 0;
             int mt, nt;
-            for (int t = static_cast<int>(pair); cur.seek(p, t, mt, nt); t += static_cast<int>(npairs)) {
-                for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+            auto mma_tile = [&](int kb0, int kb1) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const uint32_t stage = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1u;
                     const uint32_t buf = it % NBUF;
@@ -786,22 +871,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                     mma_commit_pair(&empty[stage], 0x3);
                     mma_commit_pair(&tfull[buf], 0x3);
                 }
-            }
+            };
+            int v = static_cast<int>(pair);
+            for (; v < p.dp_tiles && cur.seek(p, v, mt, nt); v += static_cast<int>(npairs)) mma_tile(0, p.num_kb);
+            int sp, kb0, kb1;
+            for (; cur.seek(p, work_item(p, v, sp, kb0, kb1), mt, nt); v += static_cast<int>(npairs))
+                mma_tile(kb0, kb1);
             // the peer's last remote arrivals must land before the barriers go away
             for (uint32_t j = 0; j < NBUF && j < it; ++j) {
                 const uint32_t i = it - 1 - j;
                 mbar_wait(&tempty[i % NBUF], (i / NBUF) & 1u);
             }
         }
-    } else if ((warp == 2 || warp == 3) && !p.out_f32 && p.splits == 1 && EPI_COLS == 128) {
+    } else if ((warp == 2 || warp == 3) && !p.out_f32 && EPI_COLS == 128) {
         // ------------------------------------------------------------ store warps (BF16)
-        // (only where promote_tile parks BF16 slices for them: 128 columns per half)
+        // (only where promote_tile parks BF16 slices for them: 128 columns per half, whole
+        // tiles; the split tail tiles are stored by the promotion warps)
         const int h = warp - 2;
         TileCursor<2 * BM, PAIR_RASTER_GM> cur;
         cur.init(p);
         uint32_t tile_no = 0;
         int mt, nt;
-        for (int t = static_cast<int>(pair); cur.seek(p, t, mt, nt); t += static_cast<int>(npairs)) {
+        for (int t = static_cast<int>(pair); t < p.dp_tiles && cur.seek(p, t, mt, nt);
+             t += static_cast<int>(npairs)) {
             const int64_t col0 = int64_t(nt) * PAIR_BN + h * EPI_COLS;
             if (col0 >= p.n) continue;
             store_tile_half(p, smEpi, h, lane, cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM,
@@ -820,22 +912,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         cur.init(p);
         uint32_t it = 0;
         uint32_t tile_no = 0;
-        auto make_tile = [&](int mt, int nt) {
+        int sp = 0, kb0 = 0, kb1 = 0;
+        auto make_tile = [&](int tq, int mt, int nt) {
+            const bool split = tq >= p.dp_tiles;
             return EpiTile{cur.row0 + int64_t(mt) * 2 * BM + int64_t(rank) * BM + r_in_tile,
-                           int64_t(cur.row0) + cur.rows, int64_t(nt) * PAIR_BN + h * EPI_COLS, cur.g, 0, p.num_kb,
-                           0, 0};
+                           int64_t(cur.row0) + cur.rows, int64_t(nt) * PAIR_BN + h * EPI_COLS, cur.g, kb0, kb1,
+                           split ? (tq - p.dp_tiles) * 2 + static_cast<int>(rank) : 0, sp, split ? p.splits : 1};
         };
         int mt = 0, nt = 0;
-        int t = static_cast<int>(pair);
-        bool have = cur.seek(p, t, mt, nt);
-        EpiTile tile = have ? make_tile(mt, nt) : EpiTile{0, 0, 0, 0, 0, 0, 0, 0};
+        int t = static_cast<int>(pair);  // work item (pair_item)
+        int tq = work_item(p, t, sp, kb0, kb1);
+        bool have = cur.seek(p, tq, mt, nt);
+        EpiTile tile = have ? make_tile(tq, mt, nt) : EpiTile{0, 0, 0, 0, 0, 0, 0, 0, 1};
         ScalePre pre = prefetch_scales(p, tile);
         while (have) {
             const int tn = t + static_cast<int>(npairs);
-            const bool have_next = cur.seek(p, tn, mt, nt);
-            const EpiTile next = have_next ? make_tile(mt, nt) : tile;
+            tq = work_item(p, tn, sp, kb0, kb1);
+            const bool have_next = cur.seek(p, tq, mt, nt);
+            const EpiTile next = have_next ? make_tile(tq, mt, nt) : tile;
             ScalePre next_pre = pre;
-            promote_tile<PAIR_BN, NBUF, true>(p, &tmD, stg, tile, pre, have_next, next, next_pre, tmem, qd,
+            promote_tile<PAIR_BN, NBUF, true>(p, &tmD, stg, smem, fixbar, tile, pre, have_next, next, next_pre, tmem, qd,
                                               h, lane, tfull, tempty, it, stg_full, stg_empty, tile_no);
             tile = next;
             pre = next_pre;
@@ -898,34 +994,85 @@ cudaError_t device_info(int& sms) {
     return cudaSuccess;
 }
 
-// Split-K plan for the one-CTA kernel (BN = 256) on small-M dense problems: choose S (slices
-// of the K loop per tile) minimising the busiest CTA's share ceil(tiles*S/sms)/S of one tile's
-// k-loop, ties to fewer slices; S = 1 when the tiles already fill the machine.
-int plan_splits(int64_t m, int64_t n, int64_t k, int sms) {
-    const int64_t tiles = ((m + BM - 1) / BM) * ((n + 255) / 256);
+// Split-K plans (BN = 256 tiles).  Work items: whole tiles [0, dp_tiles), then `splits` K slices
+// of each of the remaining split_tiles tiles (work_item); a split tile's slices park fp32
+// partials in the workspace and the last slice to arrive sums them in slice order
+// (deterministic).  Two forms:
+//  * decode (one-CTA kernel, M <= 16): every tile split, S minimising the busiest CTA's share
+//    ceil(tiles * S / sms) / S of one tile's k-loop (ties to fewer slices), when the tiles fill
+//    at most half the SMs;
+//  * tail wave (CTA pair, M >= 1024): T tiles on U units (CTA pairs) run in
+//    ceil(T / U) waves, the last R = T mod U tiles wide (pair: qkv at M = 8192 768 = 10 x 74 + 28;
+//    a P = 8 qkv shard 96 = 74 + 22; a 30B o_proj shard 32 < 74).  The first T - R tiles stay
+//    whole, the last R are cut into S = min(U / R, num_kb / 16, 8) slices, so the tail takes
+//    1/S of a tile's k-loop instead of one.  Dev A/B: FP8Q_TAIL_SPLIT=0.
+struct SplitPlan {
+    int splits = 1;
+    int dp_tiles = 0x7fffffff;
+    int64_t split_tiles = 0;
+    int ctas = 1;  // CTAs per tile (2: CTA pair, each parks its own 128 rows)
+    bool bulk = false;  // every CTA (pair) gets at most one slice, as its last work item
+};
+SplitPlan plan_split(int64_t m, int64_t n, int64_t k, int sms, bool pair) {
+    static const bool tail_enabled = [] {
+        const char* e = std::getenv("FP8Q_TAIL_SPLIT");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    SplitPlan sp;
+    sp.ctas = pair ? 2 : 1;
+    const int64_t tile_rows = pair ? 2 * BM : BM;
+    const int64_t tiles = ((m + tile_rows - 1) / tile_rows) * ((n + 255) / 256);
+    const int64_t units = pair ? sms / 2 : sms;
     const int64_t num_kb = k / BK;
-    if (tiles <= 0 || tiles * 2 > sms || num_kb < 2) return 1;
-    // measured (tools/kernel_bench.py --decode): splitting pays only for the smallest M, where
-    // the parked fp32 partials are tiny; from M ~ 32 the fixup costs more than it recovers
-    if (m > 16) return 1;
-    int best = 1;
-    double best_cost = 1e30;
-    for (int sp = 1; sp <= 16 && 2 * sp <= num_kb; ++sp) {
-        const double cost = static_cast<double>((tiles * sp + sms - 1) / sms) / sp;
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = sp;
+    if (tiles <= 0 || units <= 0 || m <= 0) return sp;
+    if (!pair && m <= 16) {
+        // measured (tools/kernel_bench.py --decode): the all-tiles split pays only for the
+        // smallest M, where the parked fp32 partials are tiny
+        if (tiles * 2 > sms || num_kb < 2) return sp;
+        int best = 1;
+        double best_cost = 1e30;
+        for (int s = 1; s <= 16 && 2 * s <= num_kb; ++s) {
+            const double cost = static_cast<double>((tiles * s + sms - 1) / sms) / s;
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = s;
+            }
         }
+        if (best > 1) {
+            sp.splits = best;
+            sp.dp_tiles = 0;
+            sp.split_tiles = tiles;
+        }
+        return sp;
     }
-    return best;
+    // measured (tools/one_shape.py, graph timings, split vs FP8Q_TAIL_SPLIT=0, two boxes): the
+    // fixup costs a few microseconds (park 128 KB per CTA, the last slice bulk-reads S x 128 KB),
+    // so it pays on the CTA pair with long slices and many m-tiles -- at M = 8192 N = 768 / 256
+    // / 1536 (K = 4096) 37.5 -> 36.4 / 21.8 -> 20.7 / 56.9 -> 53.0 us, (2048, 512, 4096) 22.1 ->
+    // 19.7, down_proj P = 2 shard (8192, 2048, 12288) 201.7 -> 187.4 -- and loses with
+    // 5-8 k-block slices (K = 2048: (8192, 640, 2048) 27.1 -> 30.0, (8192, 1280, 2048) 31.6 ->
+    // 33.4), at M = 256 (gate_up 38.3 -> 39.6) and on the one-CTA kernel ((200, 24576, 2048):
+    // 24.6 -> 26.3); those stay unsplit.
+    if (!tail_enabled || !pair || m < 8 * BM) return sp;
+    const int64_t r = tiles % units;
+    if (r == 0) return sp;
+    // one slice per unit at most (R S <= U), so every slice is its CTA's last item and the
+    // fixup can use the idle shared-memory ring; >= 16 k-blocks per slice
+    const int64_t s = std::min<int64_t>(std::min<int64_t>(units / r, num_kb / 16), 8);
+    if (s < 2) return sp;
+    sp.bulk = true;
+    sp.splits = static_cast<int>(s);
+    sp.dp_tiles = static_cast<int>(tiles - r);
+    sp.split_tiles = r;
+    return sp;
 }
-// Workspace: [counters: SPLIT_COUNTER_BYTES][partials]; the counter region sits at a fixed
-// offset so the "left zeroed" invariant holds whatever shape used the workspace before.
-constexpr size_t SPLIT_COUNTER_BYTES = 4096;  // >= 4 B x the most tiles that ever split (sms / 2)
-size_t split_ws_bytes(int64_t m, int64_t n, int sp) {
-    if (sp <= 1) return 0;
-    const int64_t tiles = ((m + BM - 1) / BM) * ((n + 255) / 256);
-    return SPLIT_COUNTER_BYTES + static_cast<size_t>(tiles * sp * BM * 256) * 4;
+// Workspace: [counters: SPLIT_COUNTER_BYTES][partials [split tile][slice][cta][128][256] fp32];
+// the counter region sits at a fixed offset so the "left zeroed" invariant holds whatever shape
+// used the workspace before.
+constexpr size_t SPLIT_COUNTER_BYTES = 4096;  // >= 4 B x split_tiles x ctas (<= sms)
+size_t split_ws_bytes(const SplitPlan& sp) {
+    if (sp.splits <= 1) return 0;
+    return SPLIT_COUNTER_BYTES + static_cast<size_t>(sp.split_tiles * sp.splits * sp.ctas * BM * 256) * 4;
 }
 
 // Kernel choice (see launch_cfg): env FP8Q_GEMM_KIND = 256 | 1256 overrides (dev only).
@@ -1008,6 +1155,8 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
     p.splits = 1;
     p.ws = nullptr;
     p.counters = nullptr;
+    p.dp_tiles = 0x7fffffff;
+    p.fix_bulk = 0;
     {
         // raster band: as many m-tiles as keep the band's A panel (rows x K bytes) within
         // ~32 MB of L2, so B streams from HBM once per band (FP8Q_GEMM_RASTER overrides, dev)
@@ -1033,30 +1182,29 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
             a.n * a.k <= (64LL << 20))
             p.raster = -p.num_n_tiles;
     }
-    if (!kPair && KIND == 256 && a.offsets == nullptr) {
-        const int sp = plan_splits(a.m, a.n, a.k, sms);
-        const size_t need = split_ws_bytes(a.m, a.n, sp);
-        if (sp > 1 && a.workspace != nullptr && a.workspace_bytes >= need) {
-            p.splits = sp;
+    // work items (whole tiles, then split slices) of a dense problem
+    int64_t items = ((a.m + (kPair ? 2 * BM : BM) - 1) / (kPair ? 2 * BM : BM)) * p.num_n_tiles;
+    if (BN == 256 && a.offsets == nullptr) {
+        const SplitPlan sp = plan_split(a.m, a.n, a.k, sms, kPair);
+        const size_t need = split_ws_bytes(sp);
+        if (sp.splits > 1 && a.workspace != nullptr && a.workspace_bytes >= need) {
+            p.splits = sp.splits;
+            p.dp_tiles = sp.dp_tiles;
             p.counters = static_cast<int32_t*>(a.workspace);
             p.ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + SPLIT_COUNTER_BYTES);
+            items = sp.dp_tiles + sp.split_tiles * sp.splits;
+            p.fix_bulk = sp.bulk ? 1 : 0;
         }
     }
 
     if (kPair) {
         int64_t clusters = sms / 2;
-        if (a.offsets == nullptr) {
-            const int64_t tiles = ((a.m + 2 * BM - 1) / (2 * BM)) * p.num_n_tiles;
-            clusters = tiles < clusters ? tiles : clusters;
-        }
+        if (a.offsets == nullptr) clusters = items < clusters ? items : clusters;
         fp8_block_gemm_pair_kernel<BN><<<static_cast<unsigned>(2 * clusters), NUM_THREADS, PairCfg<BN>::SMEM_BYTES,
                                          stream>>>(tmA, tmB, tmD, p);
     } else {
         int64_t grid = sms;
-        if (a.offsets == nullptr) {
-            const int64_t items = ((a.m + BM - 1) / BM) * p.num_n_tiles * p.splits;
-            grid = items < sms ? items : sms;
-        }
+        if (a.offsets == nullptr) grid = items < sms ? items : sms;
         fp8_block_gemm_kernel<BN><<<static_cast<unsigned>(grid), NUM_THREADS, Cfg<BN>::SMEM_BYTES, stream>>>(
             tmA, tmB, tmD, p);
     }
@@ -1071,8 +1219,8 @@ size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped) {
     if (grouped || m <= 0 || n <= 0 || k <= 0) return 0;
     int sms = 0;
     if (device_info(sms) != cudaSuccess) sms = 148;
-    if (m >= 2 * BM) return 0;  // the CTA-pair kernel does not split K
-    size_t need = split_ws_bytes(m, n, plan_splits(m, n, k, sms));
+    // the kernel choose_kind makes by default: the CTA pair from M = 256
+    size_t need = split_ws_bytes(plan_split(m, n, k, sms, m >= 2 * BM));
     if (m <= kSkinnyMaxM) need = std::max(need, skinny_workspace_bytes(m, n, k));
     return need;
 }

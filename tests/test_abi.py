@@ -83,7 +83,11 @@ def test_validation_paths_without_gpu(lib):
     assert lib.fp8_block_gemm(fake, 136, fake, 4, fake, 128, fake, 1, fake, 16, 0, 4, 16, 128, None, 0, None) == 3
     assert lib.fp8_block_gemm_grouped(fake, 128, fake, 4, fake, 128, 2048, fake, 1, 1, fake, 16, 0,
                                       4, 16, 128, fake, -1, None, 0, None) == 2
-    assert lib.fp8_block_gemm_workspace_size(8192, 6144, 4096) == 0  # prefill: no split-K
+    # prefill: only the tail wave splits (148 SMs / 74 CTA pairs; gemm.cu plan_split).  o_proj:
+    # 512 pair tiles = 6 x 74 + 68, 74 // 68 = 1 slice -> no split; qkv: 768 = 10 x 74 + 28 ->
+    # 2 slices of 28 tiles, each parking 2 CTAs x 128 x 256 fp32 behind a 4 KB counter region
+    assert lib.fp8_block_gemm_workspace_size(8192, 4096, 4096) == 0
+    assert lib.fp8_block_gemm_workspace_size(8192, 6144, 4096) == 4096 + 28 * 2 * 2 * 128 * 256 * 4
     # NEXT-3 KV cache: ld < cols -> EINVAL; identity slots with rows > num_slots -> ESHAPE;
     # misaligned amax / scale -> EALIGN; empty -> OK
     assert lib.kv_amax_update(fake, 4, 1024, 512, fake, None, None) == 1

@@ -1,6 +1,10 @@
 """bench.py's end-to-end pipeline (host inputs, chunked uploads / GEMMs / read-backs, per-tensor
-sync) must produce exactly the device-resident step's outputs: same quantizers, same GEMM per
-row (row blocks of a GEMM are independent), so the read-back BF16 outputs are bitwise equal."""
+sync) must produce the device-resident step's outputs: same quantizers, same GEMM per row (row
+blocks of a GEMM are independent), so the read-back BF16 outputs are bitwise equal -- except
+where one of the two GEMM calls cuts its tail-wave tiles into K slices (gemm.cu plan_split: it
+depends on the tile count, i.e. on M), which changes the fp32 summation order: there the BF16
+outputs agree to one BF16 ulp (plus fp32
+reordering error on cancelling sums)."""
 import pytest
 import torch
 
@@ -23,8 +27,19 @@ def test_e2e_pipeline_equals_device_step(m, chunks):
     st.run_e2e(chunks=chunks)
     torch.cuda.synchronize()
     st.engine.check_finite()
+    from paper_2601_18150_b200 import fp8q
+    lib = fp8q.load_library()
     for name, y in ref.items():
         got, want = st.h_y[name], y.cpu()
+        n, kk = y.shape[1], st.xq[name].shape[1]
+        if lib.fp8_block_gemm_workspace_size(m, n, kk) != lib.fp8_block_gemm_workspace_size(m // chunks, n, kk):
+            gf, wf = got.float(), want.float()
+            ulp = torch.ldexp(torch.ones_like(wf), torch.frexp(wf.abs().clamp_min(1e-30))[1] - 8)
+            # one BF16 ulp, plus fp32 reordering error for cancelling sums (relative to the row)
+            tol = ulp + 1e-5 * wf.abs().amax(dim=1, keepdim=True)
+            assert ((gf - wf).abs() <= tol).all(), (name, float(((gf - wf).abs() - tol).max()))
+            assert (gf != wf).float().mean().item() < 0.01, name
+            continue
         bad = (got.view(torch.int16) != want.view(torch.int16))
         if bad.any():
             rows = bad.any(dim=1).nonzero().flatten()

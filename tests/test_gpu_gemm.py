@@ -373,3 +373,53 @@ def test_gemm_forced_kinds(kind):
     r = subprocess.run([sys.executable, "-c", _KIND_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "kind ok" in r.stdout, r.stdout + r.stderr
+
+
+def _unsplit_dev(xq, xs, wq, ws):
+    """fp8_block_gemm through the C-ABI with no workspace (never splits K), F32 output."""
+    m, k = xq.shape
+    n = wq.shape[0]
+    lib = fp8q.load_library()
+    y = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    st = lib.fp8_block_gemm(xq.data_ptr(), k, xs.data_ptr(), xs.stride(0), wq.data_ptr(), k,
+                            ws.data_ptr(), ws.stride(0), y.data_ptr(), n, 1, m, n, k, None, 0,
+                            torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert st == 0
+    return y
+
+
+@pytest.mark.parametrize("m,n,k", [(8192, 768, 4096), (2048, 512, 12288), (8192, 6144, 4096),
+                                   (1100, 1000, 4096), (8192, 256, 4096), (4096, 384, 4096)])
+def test_tail_split(m, n, k):
+    # Tail-wave split of the CTA-pair kernel (gemm.cu plan_split): the last T mod 74 tiles are cut
+    # into K slices whose fp32 partials the last slice sums in slice order (bulk-copied through
+    # the idle shared-memory ring).  Ragged rows / columns: (1100, 1000).  Every element against the unsplit
+    # kernel (equal up to fp32 summation order), sampled rows against the oracle, deterministic,
+    # BF16 = RNE(F32) (whole tiles through the store warps, split tiles stored directly), and
+    # the workspace left zeroed (the second call reuses it).
+    lib = fp8q.load_library()
+    assert lib.fp8_block_gemm_workspace_size(m, n, k) > 0
+    wb = synth.qwen3_weight(n, k, 13)
+    xb = synth.qwen3_activation(m, k, 14)
+    wq, ws = fp8q.quantize_weight_blockwise(to_dev_bf16(wb))
+    xq, xs = fp8q.quantize_act_per_token_group(to_dev_bf16(xb))
+    y = fp8q.fp8_block_gemm(xq, xs, wq, ws, out_dtype=torch.float32)
+    yb = fp8q.fp8_block_gemm(xq, xs, wq, ws, out_dtype=torch.bfloat16)
+    y2 = fp8q.fp8_block_gemm(xq, xs, wq, ws, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int32), y2.view(torch.int32))
+    assert torch.equal(yb.view(torch.int16), y.to(torch.bfloat16).view(torch.int16))
+    yu = _unsplit_dev(xq, xs, wq, ws)
+    assert torch.isfinite(y).all()
+    d = (y.double() - yu.double()).norm() / yu.double().norm()
+    assert d <= 1e-6, float(d)
+    # per 256-row band: a wrong or missing slice shows up as a whole band off
+    for r0 in range(0, m, 256):
+        nb = (y[r0:r0 + 256].double() - yu[r0:r0 + 256].double()).norm()
+        assert nb <= 1e-6 * max(float(yu[r0:r0 + 256].double().norm()), 1e-30), (r0, float(nb))
+    rows = np.unique(np.r_[0, m - 1, np.random.default_rng(m + n).integers(0, m, 16)])
+    oa, osa = oracle.quantize_act_per_token_group(xb[rows])
+    ow, osw = oracle.quantize_weight_blockwise(wb)
+    ref = oracle.gemm_rows(oa, osa, ow, osw)
+    assert rel_frobenius(y[torch.from_numpy(rows).cuda()].cpu().numpy(), ref) <= 1e-5
