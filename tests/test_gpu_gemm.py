@@ -423,3 +423,33 @@ def test_tail_split(m, n, k):
     ow, osw = oracle.quantize_weight_blockwise(wb)
     ref = oracle.gemm_rows(oa, osa, ow, osw)
     assert rel_frobenius(y[torch.from_numpy(rows).cuda()].cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("m,n,k", [(1100, 1000, 4096), (8192, 768, 4096)])
+def test_tail_split_bounds(m, n, k):
+    # compute-sanitizer is closed on this pool, so the split path's memory footprint is checked
+    # directly: an exact-size workspace followed by a canary, an output with guard rows, and the
+    # counter region left zeroed (the reusable-workspace invariant of include/fp8q.h).
+    lib = fp8q.load_library()
+    need = int(lib.fp8_block_gemm_workspace_size(m, n, k))
+    assert need > 0
+    wb = synth.qwen3_weight(n, k, 21)
+    xb = synth.qwen3_activation(m, k, 22)
+    wq, ws = fp8q.quantize_weight_blockwise(to_dev_bf16(wb))
+    xq, xs = fp8q.quantize_act_per_token_group(to_dev_bf16(xb))
+    canary = 1 << 20
+    wsp = torch.zeros(need + canary, dtype=torch.uint8, device="cuda")
+    wsp[need:] = 0xA5
+    guard = 3
+    y = torch.full((m + guard, n), float("nan"), dtype=torch.float32, device="cuda")
+    st = lib.fp8_block_gemm(xq.data_ptr(), k, xs.data_ptr(), xs.stride(0), wq.data_ptr(), k,
+                            ws.data_ptr(), ws.stride(0), y.data_ptr(), n, 1, m, n, k, wsp.data_ptr(), need,
+                            torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert st == 0
+    assert bool((wsp[need:] == 0xA5).all())              # nothing written past the workspace
+    assert bool((wsp[:4096] == 0).all())                  # split counters left zeroed
+    assert bool(torch.isnan(y[m:]).all())                 # nothing written past row m
+    assert bool(torch.isfinite(y[:m]).all())              # every output written
+    yu = _unsplit_dev(xq, xs, wq, ws)
+    assert float((y[:m].double() - yu.double()).norm() / yu.double().norm()) <= 1e-6
