@@ -37,6 +37,21 @@ def test_linear_dynamic_equals_two_step(m, n, k):
                            ref.view(torch.int16 if dt == torch.bfloat16 else torch.int32)), (m, n, k, dt)
 
 
+@pytest.mark.parametrize("m,n,k", [(8192, 6144, 4096), (2048, 512, 12288)])
+def test_linear_dynamic_equals_two_step_tail_split(m, n, k):
+    # prefill shapes whose CTA-pair GEMM splits its tail-wave tiles along K (gemm.cu plan_split):
+    # the linear's workspace carries the split partials too, and both paths take the same plan
+    lib = fp8q.load_library()
+    assert lib.fp8_block_gemm_workspace_size(m, n, k) > 0
+    _, wq, ws = _weight(n, k, 9)
+    x = to_dev_bf16(synth.qwen3_activation(m, k, seed=5))
+    y = fp8q.fp8_linear_dynamic(x, wq, ws)
+    xq, xs = fp8q.quantize_act_per_token_group(x)
+    ref = fp8q.fp8_block_gemm(xq, xs, wq, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
+
+
 @pytest.mark.parametrize("m", [1, 7, 16])
 @pytest.mark.parametrize("n,k,launches", [(24576, 4096, 1), (4096, 4096, 1), (256, 16384, 1), (3072, 2048, 1),
                                           (24576, 8192, 2)])
