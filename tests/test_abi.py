@@ -88,6 +88,17 @@ def test_validation_paths_without_gpu(lib):
     # 2 slices of 28 tiles, each parking 2 CTAs x 128 x 256 fp32 behind a 4 KB counter region
     assert lib.fp8_block_gemm_workspace_size(8192, 4096, 4096) == 0
     assert lib.fp8_block_gemm_workspace_size(8192, 6144, 4096) == 4096 + 28 * 2 * 2 * 128 * 256 * 4
+    # the tail plan (S = min(74 // R, k-blocks // 16, 8), CTA pair, M >= 1024) on the shapes
+    # DESIGN §5.2 names: R tail tiles x S slices x 2 CTAs x 128 KB behind the counters
+    part = 2 * 128 * 256 * 4
+    for (m, n, k), (r, sl) in {(8192, 768, 4096): (22, 2), (8192, 2048, 12288): (34, 2),
+                               (2048, 512, 12288): (16, 4), (8192, 256, 4096): (32, 2)}.items():
+        assert lib.fp8_block_gemm_workspace_size(m, n, k) == 4096 + r * sl * part, (m, n, k)
+    for m, n, k in [(256, 24576, 4096),   # M < 1024: measured slower split (decode gate_up)
+                    (8192, 640, 2048),    # K = 2048: slices under 16 k-blocks
+                    (8192, 24576, 4096),  # 3072 = 41 x 74 + 38: 74 // 38 = 1
+                    (8192, 4096, 12288)]:  # 512 = 6 x 74 + 68
+        assert lib.fp8_block_gemm_workspace_size(m, n, k) == 0, (m, n, k)
     # NEXT-3 KV cache: ld < cols -> EINVAL; identity slots with rows > num_slots -> ESHAPE;
     # misaligned amax / scale -> EALIGN; empty -> OK
     assert lib.kv_amax_update(fake, 4, 1024, 512, fake, None, None) == 1
