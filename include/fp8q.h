@@ -216,8 +216,8 @@ fp8q_status silu_mul_quantize_act_per_token_group(const void* gate_up_bf16, int6
  *           shared memory) and never touch the workspace.
  *   Kernels: 1 <= m <= 128 with 16-byte-aligned a_scales and ld_sa % 4 == 0 runs the swap-AB
  *     decode kernel (weight rows in the MMA M dimension, tokens in N), and so does
- *     129 <= m <= 256 where its cluster split-K applies; otherwise the 128 x 256 / 256 x 256
- *     (CTA pair) tile kernel.  All compute the same per-k-block promotion in the same k order
+ *     129 <= m <= 256 where its cluster split-K applies and the CTA pair would not split its
+ *     tiles along K over most SMs; otherwise the 128 x 256 / 256 x 256 (CTA pair) tile kernel.  All compute the same per-k-block promotion in the same k order
  *     (split-K partial sums are added in a fixed order: results are deterministic).
  *   Requirements: k % 128 == 0, n % 8 == 0 (ESHAPE); a, b 16-byte aligned with ld_a % 16 ==
  *     0 and ld_b % 16 == 0 (TMA); d 16-byte aligned with ld_d * sizeof(out) % 16 == 0;

@@ -1053,13 +1053,18 @@ SplitPlan plan_split(int64_t m, int64_t n, int64_t k, int sms, bool pair) {
     // 5-8 k-block slices (K = 2048: (8192, 640, 2048) 27.1 -> 30.0, (8192, 1280, 2048) 31.6 ->
     // 33.4), at M = 256 (gate_up 38.3 -> 39.6) and on the one-CTA kernel ((200, 24576, 2048):
     // 24.6 -> 26.3); those stay unsplit.
-    if (!tail_enabled || !pair || m < 8 * BM) return sp;
+    if (!tail_enabled || !pair || m < 2 * BM) return sp;
     const int64_t r = tiles % units;
     if (r == 0) return sp;
     // one slice per unit at most (R S <= U), so every slice is its CTA's last item and the
     // fixup can use the idle shared-memory ring; >= 16 k-blocks per slice
     const int64_t s = std::min<int64_t>(std::min<int64_t>(units / r, num_kb / 16), 8);
     if (s < 2) return sp;
+    // below M = 1024 only without a whole wave and with the slices on >= 64 % of the SMs: then
+    // the split pair beats the swap-AB cluster kernel at decode M = 256 (measured, one box:
+    // down_proj 31.0 -> 27.7 us on 128 SMs, qkv 23.9 -> 21.0 on 96; o_proj, 64 SMs, 16.9 ->
+    // 20.6 stays on the cluster kernel; gate_up, one whole wave + 22 tiles, 38.3 -> 38.4)
+    if (m < 8 * BM && !(tiles < units && 100 * (2 * r * s) >= 64 * sms)) return sp;
     sp.bulk = true;
     sp.splits = static_cast<int>(s);
     sp.dp_tiles = static_cast<int>(tiles - r);
@@ -1214,6 +1219,13 @@ cudaError_t launch_cfg(const GemmArgs& a, PFN_cuTensorMapEncodeTiled_v12000 enco
 }  // namespace
 
 void* tensor_map_encode_fn() { return reinterpret_cast<void*>(tensor_map_encoder()); }
+
+bool pair_tail_split_applies(int64_t m, int64_t n, int64_t k, size_t workspace_bytes) {
+    int sms = 0;
+    if (m < 2 * BM || device_info(sms) != cudaSuccess) return false;
+    const SplitPlan sp = plan_split(m, n, k, sms, true);
+    return sp.splits > 1 && workspace_bytes >= split_ws_bytes(sp);
+}
 
 size_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, bool grouped) {
     if (grouped || m <= 0 || n <= 0 || k <= 0) return 0;

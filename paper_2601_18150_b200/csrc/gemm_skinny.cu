@@ -969,6 +969,8 @@ bool skinny_gemm_applies(const GemmArgs& a) {
     // spread (gate_up), this one where the tile kernel would leave most SMs idle (qkv, o, down).
     if (a.m > 128) {  // M = 129..256: only as cluster split-K (few weight tiles, e.g. o/down/qkv)
         if (forced == 16) return true;
+        // ... unless the CTA pair splits its tiles along K over most SMs (M = 256: qkv, down)
+        if (a.workspace != nullptr && pair_tail_split_applies(a.m, a.n, a.k, a.workspace_bytes)) return false;
         int sms = 0;
         if (sk_device_info(sms) != cudaSuccess) return false;
         return sk_cluster_size<256>(static_cast<int>((a.n + SK_BN - 1) / SK_BN), static_cast<int>(a.k / SK_BK), sms) >= 2;

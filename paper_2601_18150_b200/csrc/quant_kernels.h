@@ -81,6 +81,9 @@ bool skinny_fused_act_applies(const GemmArgs& a);
 // (m > 128 only where its cluster split-K mode applies).
 constexpr int kSkinnyMaxM = 256;
 bool skinny_gemm_applies(const GemmArgs& a);
+// The CTA-pair kernel would split its tail-wave tiles along K for this dense shape (gemm.cu
+// plan_split); at decode M = 256 that wins over the swap-AB kernel, which then steps aside.
+bool pair_tail_split_applies(int64_t m, int64_t n, int64_t k, size_t workspace_bytes);
 size_t skinny_workspace_bytes(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_fp8_gemm_skinny(const GemmArgs& a, void* encode_fn, cudaStream_t stream);
 

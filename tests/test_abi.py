@@ -92,9 +92,11 @@ def test_validation_paths_without_gpu(lib):
     # DESIGN §5.2 names: R tail tiles x S slices x 2 CTAs x 128 KB behind the counters
     part = 2 * 128 * 256 * 4
     for (m, n, k), (r, sl) in {(8192, 768, 4096): (22, 2), (8192, 2048, 12288): (34, 2),
-                               (2048, 512, 12288): (16, 4), (8192, 256, 4096): (32, 2)}.items():
+                               (2048, 512, 12288): (16, 4), (8192, 256, 4096): (32, 2),
+                               (256, 4096, 12288): (16, 4), (256, 6144, 4096): (24, 2)}.items():
         assert lib.fp8_block_gemm_workspace_size(m, n, k) == 4096 + r * sl * part, (m, n, k)
-    for m, n, k in [(256, 24576, 4096),   # M < 1024: measured slower split (decode gate_up)
+    for m, n, k in [(256, 24576, 4096),   # M < 1024 with a whole wave: no gain (decode gate_up)
+                    (256, 4096, 4096),    # M < 1024, slices on 64 SMs: the cluster kernel wins
                     (8192, 640, 2048),    # K = 2048: slices under 16 k-blocks
                     (8192, 24576, 4096),  # 3072 = 41 x 74 + 38: 74 // 38 = 1
                     (8192, 4096, 12288)]:  # 512 = 6 x 74 + 68

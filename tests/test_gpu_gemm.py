@@ -390,11 +390,14 @@ def _unsplit_dev(xq, xs, wq, ws):
 
 
 @pytest.mark.parametrize("m,n,k", [(8192, 768, 4096), (2048, 512, 12288), (8192, 6144, 4096),
-                                   (1100, 1000, 4096), (8192, 256, 4096), (4096, 384, 4096)])
+                                   (1100, 1000, 4096), (8192, 256, 4096), (4096, 384, 4096),
+                                   (256, 4096, 12288), (256, 6144, 4096)])
 def test_tail_split(m, n, k):
     # Tail-wave split of the CTA-pair kernel (gemm.cu plan_split): the last T mod 74 tiles are cut
     # into K slices whose fp32 partials the last slice sums in slice order (bulk-copied through
-    # the idle shared-memory ring).  Ragged rows / columns: (1100, 1000).  Every element against the unsplit
+    # the idle shared-memory ring).  Ragged rows / columns: (1100, 1000).  Decode M = 256 down /
+    # qkv: the split pair replaces the swap-AB cluster kernel (the unsplit reference, called
+    # without a workspace, runs the latter).  Every element against the unsplit
     # kernel (equal up to fp32 summation order), sampled rows against the oracle, deterministic,
     # BF16 = RNE(F32) (whole tiles through the store warps, split tiles stored directly), and
     # the workspace left zeroed (the second call reuses it).
